@@ -1,0 +1,398 @@
+#!/usr/bin/env python
+"""bench.py — batched symmetric-stair PCG on B200 (BASELINE.json config c4).
+
+A "step" = one pass of the hot path (K1 Schur formation -> K3 persistent
+symmetric-stair PCG, fp64, eps 1e-8, lambda0 = 0) over one batch of 4096
+independent synthetic iiwa-like KKT systems (K = 64 knots, nx = 14, nu = 7)
+per GPU. Weak scaling: every rank owns its own 4096 systems (contiguous
+batch-index shard, seeds seed0 + global index), no inter-GPU traffic.
+
+  value : batched solves/s, whole job, inputs resident in HBM
+          (CUDA events on the launch stream, max over ranks)
+  e2e   : same metric through the host-buffer C-ABI call b2p_solve_batched
+          (pinned host KKT in, H2D + solve + D2H of lambda + status inside
+          the timed region)
+Also reported: single-solve latency (c1) and PCG iterations.
+
+--impl reference: the reference's CPU implementation of the path (the
+oracle restatement; the reference cannot be compiled here)
+on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2309_08079_b200.types import PcgConfig, PrecondKind  # noqa: E402
+
+METRIC = "batched PCG solves/s (symmetric-stair, fp64)"
+UNIT = "solves/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=4096, help="systems per GPU")
+    ap.add_argument("--knots", type=int, default=64)
+    ap.add_argument("--nx", type=int, default=14)
+    ap.add_argument("--nu", type=int, default=7)
+    ap.add_argument("--eps", type=float, default=1e-8)
+    ap.add_argument("--seed", type=int, default=2309)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="CPU baseline sample budget (seconds)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    return ap.parse_args()
+
+
+def workload(a):
+    return {
+        "workload": (f"c4: {a.batch} independent synthetic iiwa-like KKT systems per GPU "
+                     f"(random_kkt, seeds seed0+i), K={a.knots} knots (N={a.knots - 1}), "
+                     f"nx={a.nx}, nu={a.nu}; build_schur + symmetric-stair build + PCG to "
+                     f"eps={a.eps:g}, lambda0=0"),
+        "batch_per_gpu": a.batch, "knots": a.knots, "nx": a.nx, "nu": a.nu,
+        "precond": "symstair", "epsilon": a.eps, "dtype": "fp64",
+        "l2": "inputs larger than L2 (1.19 GB per GPU vs 126 MB L2)",
+        "parallelism": "batch-index shards, one process per GPU",
+    }
+
+
+# ------------------------------------------------------------------ helpers
+def kkt_bytes(N, n, m, w=8):
+    K = N + 1
+    return w * (K * n * n + K * n + N * m * m + N * m + N * n * n + N * n * m + N * n + 2 * n)
+
+
+def algorithmic(N, n, m, iters, w=8):
+    """Per-system algorithmic bytes / flops."""
+    K = N + 1
+    nn = n * n
+    b_in = kkt_bytes(N, n, m, w)
+    b_k1 = b_in + w * (3 * K * nn + K * nn + K * n)      # read KKT, write S, theta^-1, gamma
+    b_k3 = w * (3 * K * nn + K * nn + K * n + K * n)     # read S, theta^-1, gamma; write lambda
+    b_full = b_in + 2 * K * n * w                         # compulsory: KKT in, lambda0 + lambda
+    f_form = (K - 1) * (17 * n ** 3 + 2.33 * m ** 3 + 2 * n * m * (n + m)) + 2.33 * n ** 3
+    f_iter = 4 * (3 * K - 2) * nn + 10 * K * n
+    return dict(b_in=b_in, b_k1=b_k1, b_k3=b_k3, b_full=b_full, f_form=f_form,
+                f_iter=f_iter, f_full=f_form + (iters + 1) * f_iter)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_sample(a, seconds, seed0):
+    """Oracle (restated reference) on all host threads over a bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as orc
+    import paper_2309_08079_b200.api as api  # host-side generator only
+    orc.build()
+    threads = os.cpu_count() or 1
+    N = a.knots - 1
+    cfg = PcgConfig(epsilon=a.eps)
+    # calibrate with a small batch, then size the sample for ~`seconds`
+    cal = max(threads, 8)
+    kb = api.random_kkt_batch(seed0, cal, N, a.nx, a.nu)
+    secs, _, reps = orc.solve_batch(kb, PrecondKind.symmetric_stair, 1, cfg, threads=threads,
+                                    want_lambda=False)
+    per = secs / cal
+    sample = int(min(a.batch, max(cal, seconds / max(per, 1e-9))))
+    kb = api.random_kkt_batch(seed0, sample, N, a.nx, a.nu)
+    secs, _, reps = orc.solve_batch(kb, PrecondKind.symmetric_stair, 1, cfg, threads=threads,
+                                    want_lambda=False)
+    iters = float(np.mean([r.iterations for r in reps]))
+    return sample / secs, sample, secs, threads, iters
+
+
+def run_reference(a, world, rank):
+    if rank != 0:
+        return
+    steps, warm = a.steps, a.warmup
+    budget = max(2.0, min(20.0, 150.0 / max(1, steps + warm)))
+    for _ in range(warm):
+        cpu_sample(a, budget / 4, a.seed)
+    vals = []
+    sample = 0
+    threads = 1
+    iters = 0.0
+    t_total = 0.0
+    for s in range(steps):
+        v, sample, secs, threads, iters = cpu_sample(a, budget, a.seed)
+        vals.append(v)
+        t_total += secs
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": a.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 * t_total / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (random_kkt, seeded)",
+        "config": workload(a),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} systems of the c4 workload per step "
+                                   f"(oracle restatement of proj/src, g++ -O3, "
+                                   f"parallel_for over instances as trajopt_cli.cpp:155)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "pcg_iters_mean": iters,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_b200(a, world, rank, local):
+    import torch
+    import paper_2309_08079_b200.api as api
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = api.Context(local)
+    # one explicit stream: the library launches on it and the timing events
+    # are recorded on it (torch.cuda.Event sees only the stream it is given)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+
+    N, n, m, B = a.knots - 1, a.nx, a.nu, a.batch
+    D = (N + 1) * n
+    cfg = PcgConfig(epsilon=a.eps)
+    seed0 = a.seed + rank * B
+
+    def pinned(shape, dt):
+        return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+    kb = api.random_kkt_batch(seed0, B, N, n, m, alloc=pinned)
+    # device-resident copy (value leg)
+    dev = [torch.from_numpy(x).to(f"cuda:{local}", non_blocking=True) for x in kb.arrays()]
+    from paper_2309_08079_b200.types import KKTSystem
+    kd = KKTSystem(N, n, m, *dev)
+    lam_dev = torch.empty((B, D), dtype=torch.float64, device=f"cuda:{local}")
+    torch.cuda.synchronize()
+
+    def step():
+        api.solve_batched_device(kd, lam_dev.data_ptr(), B, PrecondKind.symmetric_stair, 1, cfg,
+                                 ctx=ctx)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def allmax(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (also validates every system once)
+    reps = api.solve_batched_device(kd, lam_dev.data_ptr(), B, PrecondKind.symmetric_stair, 1,
+                                    cfg, ctx=ctx, want_reports=True)
+    iters = [r.iterations for r in reps]
+    assert all(r.converged for r in reps), "unconverged systems in the bench batch"
+    for _ in range(max(0, a.warmup - 1)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: value (HBM-resident inputs)
+    launches0 = ctx.kernel_launches()
+    ctx.phase_accounting(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(a.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = allmax(ev0.elapsed_time(ev1))
+    k1_ms, k3_ms, tot_ms, nsolves = ctx.phase_totals()
+    ctx.phase_accounting(False)
+    launches = ctx.kernel_launches() - launches0
+    value = world * B * a.steps / (elapsed_ms * 1e-3)
+
+    # ---- e2e: host buffers through the C-ABI (pinned in, pinned out)
+    e2e = None
+    if not a.no_e2e:
+        lam_host = torch.empty((B, D), dtype=torch.float64, pin_memory=True).numpy()
+        ctx_h = api.Context(local)
+        api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg, lambda_out=lam_host, ctx=ctx_h)
+        barrier()
+        e2e_ms = 0.0
+        for _ in range(a.steps):
+            api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg, lambda_out=lam_host,
+                              ctx=ctx_h)
+            e2e_ms += ctx_h.last_solve_ms()
+        barrier()
+        e2e_ms = allmax(e2e_ms)
+        # parity spot check of the e2e output against the device leg
+        torch.cuda.synchronize()
+        assert np.array_equal(lam_host, lam_dev.cpu().numpy()), "e2e/device outputs differ"
+        import ctypes
+        sysout = 56  # sizeof(SysOut) copied back per system
+        e2e = {"value": world * B * a.steps / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": B * kkt_bytes(N, n, m),
+               "d2h_bytes_per_step": B * (D * 8 + sysout + 4),
+               "path": "b2p_solve_batched (host pinned buffers, 2-stream chunked H2D/compute/D2H)"}
+        ctx_h.close()
+
+    # ---- single-solve latency (c1: K=32 knots, n14 m7, fp64, eps 1e-8)
+    latency = None
+    if not a.no_latency and rank == 0:
+        k1 = api.random_kkt(1, 31, 14, 7)
+        c1cfg = PcgConfig(epsilon=1e-8)
+        lat = []
+        it1 = 0
+        for i in range(25):
+            r = api.solve(k1, PrecondKind.symmetric_stair, 1, c1cfg)
+            if i >= 5:
+                lat.append(r.report.wall_time * 1e6)
+            it1 = r.report.iterations
+        latency = {"c1_us_median": statistics.median(lat), "c1_us_min": min(lat),
+                   "c1_iterations": it1,
+                   "what": "device time (CUDA events) of K1+K3 for one K=32 n=14 m=7 system; "
+                           "host copies excluded"}
+
+    # ---- roofline for the dominant kernel
+    mean_iters = float(np.mean(iters))
+    alg = algorithmic(N, n, m, mean_iters)
+    hbm, peak_src = peaks()
+    k1_avg = k1_ms / max(1, nsolves)
+    k3_avg = k3_ms / max(1, nsolves)
+    dom = "K3_pcg" if k3_avg >= k1_avg else "K1_schur_formation"
+    dom_ms = max(k1_avg, k3_avg)
+    dom_bytes = B * (alg["b_k3"] if dom == "K3_pcg" else alg["b_k1"])
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    flops_step = B * alg["f_full"]
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": elapsed_ms / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (random_kkt seeded draws, the reference generator restated)",
+        "config": workload(a),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+                     "phase_ms_per_step": {"K1_schur_formation": k1_avg, "K3_pcg": k3_avg},
+                     "fp64_tflops_step": flops_step / (elapsed_ms / a.steps * 1e-3) / 1e12,
+                     "b_full_GBs": B * alg["b_full"] / (elapsed_ms / a.steps * 1e-3) / 1e9},
+        "pcg_iters": {"mean": mean_iters, "min": int(min(iters)), "max": int(max(iters))},
+        "latency": latency,
+        "clocks": clk.summary(),
+    }
+    if not a.no_cpu and world == 1 and rank == 0:
+        v, sample, secs, threads, cit = cpu_sample(a, a.cpu_seconds, a.seed)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"{sample} systems of the same workload "
+                                          f"({secs:.1f} s, oracle restatement, all host threads)",
+                                "pcg_iters_mean": cit}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    world, rank, local = dist_setup()
+    if a.impl == "reference":
+        run_reference(a, world, rank)
+    else:
+        run_b200(a, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

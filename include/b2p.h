@@ -136,7 +136,11 @@ long long b2p_ctx_kernel_launches(b2p_ctx* ctx);
 /* ---- block_tri.hpp ---------------------------------------------------- */
 /* BlockTriMatrix::matvec (block_tri.cpp:70-92). */
 int b2p_blocktri_matvec(b2p_ctx* ctx, int dtype, int K, int nb, const void* M, const void* x,
-                        void* y, b2p_error* err);
+                        int x_len, void* y, b2p_error* err);
+/* BlockTriMatrix::cholesky_solve (block_tri.cpp:121-159): the direct
+ * block-Thomas baseline (bench-pcg's "dense_baseline" row). */
+int b2p_blocktri_cholesky_solve(b2p_ctx* ctx, int dtype, int K, int nb, const void* M,
+                                const void* rhs, int rhs_len, void* x, b2p_error* err);
 /* BlockTriMatrix::max_asymmetry / max_abs (block_tri.cpp:161-177), on device. */
 int b2p_blocktri_check(b2p_ctx* ctx, int dtype, int K, int nb, const void* M,
                        double* max_asymmetry, double* max_abs, b2p_error* err);
@@ -157,17 +161,19 @@ int b2p_build_preconditioner(b2p_ctx* ctx, int dtype, int kind, int order, int K
 /* apply_preconditioner (schur.hpp:56, schur.cpp:175-194). S is only read for
  * poly_split (remainder E = Psi - S). */
 int b2p_apply_preconditioner(b2p_ctx* ctx, int dtype, int kind, int order, int K, int nb,
-                             const void* S, const void* phi_inv, const void* r, void* out,
-                             b2p_error* err);
+                             const void* S, const void* phi_inv, const void* r, int r_len,
+                             void* out, b2p_error* err);
 
 /* ---- pcg.hpp ---------------------------------------------------------- */
 /* pcg_solve / pcg_solve_block_parallel / pcg_solve_auto (pcg.hpp:57-70,
  * pcg.cpp:55-369) — dispatch on cfg->variant. trace: nullable, capacity
- * resolved max_iter. phi_inv may be NULL for identity. */
+ * resolved max_iter. phi_inv may be NULL for identity. The *_len / phi_K /
+ * phi_nb arguments carry the caller's vector and preconditioner sizes so the
+ * reference's validate_inputs messages (pcg.cpp:24-47) are reproduced. */
 int b2p_pcg_solve(b2p_ctx* ctx, int dtype, int K, int nb, const void* S, int kind, int order,
-                  const void* phi_inv, const void* gamma, const void* lambda0,
-                  const b2p_pcg_config* cfg, void* lambda_out, b2p_solve_report* report,
-                  double* trace, b2p_error* err);
+                  int phi_K, int phi_nb, const void* phi_inv, const void* gamma, int gamma_len,
+                  const void* lambda0, int lambda0_len, const b2p_pcg_config* cfg,
+                  void* lambda_out, b2p_solve_report* report, double* trace, b2p_error* err);
 
 /* ---- fused hot path (north star): build_schur -> build_preconditioner ->
  * pcg_solve_auto for one system in one device pass. lambda0 NULL => 0. ---- */
@@ -203,6 +209,16 @@ int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
 
 /* Device time (ms) of the most recent solve kernels on this context. */
 int b2p_ctx_last_solve_ms(b2p_ctx* ctx, float* ms);
+/* Per-kernel split of the most recent fused solve: ms[0] = K1 Schur
+ * formation, ms[1] = K3 PCG (CUDA events on the launch stream; n >= 2).
+ * Valid after the caller synchronised the stream. */
+int b2p_ctx_last_phase_ms(b2p_ctx* ctx, float* ms, int n);
+/* Phase accounting for measurement: while enabled every fused solve records
+ * its own (start, K1 end, K3 end) CUDA events on the launch stream;
+ * b2p_ctx_phase_totals waits for them and returns the summed K1 / K3 / total
+ * device ms (n >= 3) and the number of solves, then resets. */
+int b2p_ctx_phase_accounting(b2p_ctx* ctx, int enable);
+int b2p_ctx_phase_totals(b2p_ctx* ctx, float* ms, int n, int* count);
 
 /* ---- random_problem.hpp (host-side input synthesis) -------------------- */
 /* family: 0 random_kkt, 1 random_kkt_scaled(diag_floor, coupling),

@@ -1,0 +1,1181 @@
+// Host side of the C-ABI (include/b2p.h): contexts, validation with the
+// reference's messages, device workspaces, launch configuration and the
+// batched / multi-GPU drivers. No CPU fallback: every compute entry point
+// runs on the device or fails with B2P_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/b2p.h"
+#include "kernels.h"
+
+using namespace b2p;
+
+struct b2p_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t user = nullptr;
+  cudaStream_t aux = nullptr;  // second pipeline stream for batched host calls
+  std::map<std::string, std::pair<void*, size_t>> ws;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;  // start, end, formation end
+  bool phases = false;
+  // phase accounting: one (start, formation end, end) event triple per fused solve
+  bool accounting = false;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  float last_ms = 0.f;
+  std::atomic<long long> launches{0};
+  int sm_count = 148;
+  size_t smem_optin = 227 * 1024;
+  cudaStream_t stream() const { return user ? user : own; }
+};
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct Fail {
+  int code;
+  std::string msg;
+  int knot = -1, iteration = -1, system = -1;
+};
+
+void fill_err(b2p_error* err, const Fail& f) {
+  if (!err) return;
+  err->code = f.code;
+  err->knot = f.knot;
+  err->iteration = f.iteration;
+  err->system = f.system;
+  std::snprintf(err->message, sizeof(err->message), "%s", f.msg.c_str());
+}
+
+void clear_err(b2p_error* err) {
+  if (!err) return;
+  err->code = B2P_OK;
+  err->knot = err->iteration = err->system = -1;
+  err->message[0] = 0;
+}
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw Fail{B2P_CUDA_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e_) +    \
+                                     " at " + __FILE__ + ":" + std::to_string(__LINE__)};  \
+  } while (0)
+
+template <class F>
+int guard(b2p_error* err, F&& f) {
+  clear_err(err);
+  try {
+    f();
+    return B2P_OK;
+  } catch (const Fail& e) {
+    fill_err(err, e);
+    return e.code;
+  } catch (const std::exception& e) {
+    fill_err(err, Fail{B2P_RUNTIME_ERROR, e.what()});
+    return B2P_RUNTIME_ERROR;
+  }
+}
+
+Fail invalid(const std::string& m) { return Fail{B2P_INVALID_ARGUMENT, m}; }
+
+// std::to_string(double) == "%f"
+std::string fstr(double v) {
+  char buf[512];
+  std::snprintf(buf, sizeof(buf), "%f", v);
+  return buf;
+}
+
+size_t esize(int dtype) { return dtype == B2P_F32 ? 4 : 8; }
+
+void check_dtype(int dtype) {
+  if (dtype != B2P_F64 && dtype != B2P_F32) throw invalid("b2p: unknown dtype");
+}
+void check_ctx(b2p_ctx* ctx) {
+  if (!ctx) throw invalid("b2p: null context");
+  CK(cudaSetDevice(ctx->device));
+}
+void check_blocktri(int K, int nb) {
+  if (K < 1 || nb < 1)
+    throw invalid("BlockTriMatrix: need at least one block row and block_dim >= 1");
+  if (nb > 32) throw invalid("b2p: block_dim > 32 is not supported by the warp-tile kernels");
+}
+
+// ------------------------------------------------------------------ workspaces
+void* ws_get(b2p_ctx* c, const std::string& name, size_t bytes) {
+  auto& slot = c->ws[name];
+  if (slot.second < bytes) {
+    if (slot.first) CK(cudaFree(slot.first));
+    slot.first = nullptr;
+    slot.second = 0;
+    if (bytes) CK(cudaMalloc(&slot.first, bytes));
+    slot.second = bytes;
+  }
+  return slot.first;
+}
+
+void h2d(b2p_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+}
+void d2h(b2p_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+}
+
+// ------------------------------------------------------------------ messages
+std::string schur_msg(int key, int* knot) {
+  const int b = key / 4, call = key % 4;
+  const char* what = "Q";
+  int k = 0;
+  if (b == 0) {
+    k = 0;
+  } else {
+    k = b - 1;
+    if (call == 1) what = "R";
+    if (call == 2) k = b;  // Q_{k+1}
+    if (call == 3) what = "theta";
+  }
+  if (knot) *knot = k;
+  return std::string("build_schur: ") + what + " at knot " + std::to_string(k) +
+         " is not positive definite";
+}
+
+Fail pcg_fail(const SysOut& o) {
+  Fail f{o.code, ""};
+  f.iteration = o.iteration;
+  switch (o.which) {
+    case kWhichInitNonFinite: f.msg = "pcg: non-finite initial residual"; break;
+    case kWhichUpsNonFinite:
+      f.msg = "pcg: non-finite p'Sp at iteration " + std::to_string(o.iteration);
+      break;
+    case kWhichEtaNonFinite:
+      f.msg = "pcg: non-finite iterate at iteration " + std::to_string(o.iteration);
+      break;
+    case kWhichBreakdown:
+      f.msg = "pcg: p'Sp = " + fstr(o.value) + " at iteration " + std::to_string(o.iteration) +
+              "; S is not positive definite on the search space";
+      break;
+    default: f.msg = "pcg: device error";
+  }
+  return f;
+}
+
+void fill_report(b2p_solve_report* r, const SysOut& o, double wall) {
+  if (!r) return;
+  r->iterations = o.iterations;
+  r->converged = o.converged;
+  r->exit_eta = o.exit_eta;
+  r->wall_time = wall;
+  r->max_residual_drift = o.max_drift;
+  r->trace_len = o.trace_len;
+  r->status = o.code;
+}
+
+// ------------------------------------------------------------------ launch config
+int env_int(const char* name, int def) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : def;
+}
+
+template <class T>
+void configure_pcg(b2p_ctx* c, PcgParams<T>& p, bool allow_grid) {
+  const size_t budget = std::min<size_t>(c->smem_optin, 227 * 1024) - 2048;
+  p.nthreads = env_int("B2P_PCG_THREADS", 256);
+  const int forceG = env_int("B2P_PCG_G", 0);
+  const int forceStage = env_int("B2P_PCG_STAGE", -1);
+  auto try_cfg = [&](int G, int stage) {
+    p.G = G;
+    p.rows_per = (p.K + G - 1) / G;
+    p.G = (p.K + p.rows_per - 1) / p.rows_per;
+    p.stage = stage;
+    return pcg_smem_bytes(p) <= budget;
+  };
+  auto set_sync = [&]() {
+    p.sync = p.G == 1 ? kSyncCta : (p.G <= 16 && p.B > 1 ? kSyncCluster
+                                    : (p.G <= 8 ? kSyncCluster : kSyncGrid));
+  };
+  if (p.check_drift) {  // the drift probe is evaluated on one CTA (sequential variant)
+    if (!try_cfg(1, forceStage < 0 ? 1 : forceStage)) try_cfg(1, 0);
+    p.sync = kSyncCta;
+    return;
+  }
+  if (forceG > 0) {
+    if (!try_cfg(forceG, forceStage < 0 ? 1 : forceStage)) try_cfg(forceG, 0);
+    set_sync();
+    if (p.sync == kSyncGrid && (!allow_grid || p.B > 1)) {
+      try_cfg(1, 0);
+      p.sync = kSyncCta;
+    }
+    return;
+  }
+  if (forceStage != 0) {
+    for (int G : {1, 2, 4, 8}) {
+      if (try_cfg(G, 1)) {
+        set_sync();
+        return;
+      }
+    }
+    if (allow_grid && p.B == 1) {
+      // one solve across many SMs: cooperative grid with staged rows
+      for (int rows = 8; rows >= 1; --rows) {
+        const int G = (p.K + rows - 1) / rows;
+        if (G > c->sm_count) break;
+        if (try_cfg(G, 1)) {
+          p.sync = kSyncGrid;
+          return;
+        }
+      }
+    }
+  }
+  try_cfg(1, 0);
+  p.sync = kSyncCta;
+}
+
+template <class T>
+void pcg_common(PcgParams<T>& p, const b2p_pcg_config* cfg, int K, int nb) {
+  p.K = K;
+  p.nb = nb;
+  p.epsilon = cfg ? cfg->epsilon : 1e-4;
+  const int mi = cfg ? cfg->max_iter : 0;
+  p.max_iter = mi > 0 ? mi : K * nb;  // resolve_max_iter, pcg.cpp:49-51
+  // the drift probe exists in the sequential variant only (pcg.cpp:103-108)
+  p.check_drift = (cfg && cfg->check_residual_drift && cfg->variant == B2P_SEQUENTIAL) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ PCG runner
+template <class T>
+void run_pcg(b2p_ctx* c, PcgParams<T>& p, cudaStream_t st, bool time_it) {
+  const size_t D = static_cast<size_t>(p.K) * p.nb;
+  p.best = static_cast<T*>(ws_get(c, "pcg_best", sizeof(T) * D * p.B));
+  p.pub = static_cast<T*>(ws_get(c, "pcg_pub", sizeof(T) * D * p.B));
+  p.slots = static_cast<T*>(ws_get(c, "pcg_slots", sizeof(T) * 2 * std::max(1, p.G) * p.B + 64));
+  c->phases = false;
+  if (time_it) CK(cudaEventRecord(c->ev0, st));
+  CK(launch_pcg<T>(p, st));
+  c->launches++;
+  if (time_it) CK(cudaEventRecord(c->ev1, st));
+}
+
+// kkt views
+struct KktDev {
+  const void *Q, *q, *R, *r, *A, *B, *e, *x_s, *x0;
+};
+
+// Upload `count` systems starting at `first` from a host batch into one
+// contiguous device block; returns per-array device pointers.
+KktDev upload_kkt(b2p_ctx* c, const b2p_kkt* k, size_t esz, int first, int count, void* dst,
+                  cudaStream_t st) {
+  const size_t N = k->N, n = k->n, m = k->m, K = N + 1;
+  const size_t sz[9] = {K * n * n, K * n, N * m * m, N * m, N * n * n, N * n * m, N * n, n, n};
+  const void* src[9] = {k->Q, k->q, k->R, k->r, k->A, k->B, k->e, k->x_s, k->x0};
+  const void* out[9];
+  char* d = static_cast<char*>(dst);
+  for (int a = 0; a < 9; ++a) {
+    const size_t bytes = sz[a] * esz * count;
+    if (bytes && !src[a]) throw invalid("b2p_kkt: null array");
+    if (bytes)
+      h2d(c, d, static_cast<const char*>(src[a]) + sz[a] * esz * first, bytes, st);
+    out[a] = d;
+    d += (bytes + 255) / 256 * 256;
+  }
+  return KktDev{out[0], out[1], out[2], out[3], out[4], out[5], out[6], out[7], out[8]};
+}
+
+size_t kkt_block_bytes(const b2p_kkt* k, size_t esz, int count) {
+  const size_t N = k->N, n = k->n, m = k->m, K = N + 1;
+  const size_t sz[9] = {K * n * n, K * n, N * m * m, N * m, N * n * n, N * n * m, N * n, n, n};
+  size_t total = 0;
+  for (size_t s : sz) total += (s * esz * count + 255) / 256 * 256;
+  return total;
+}
+
+KktDev dev_view(const b2p_kkt* k) {
+  return KktDev{k->Q, k->q, k->R, k->r, k->A, k->B, k->e, k->x_s, k->x0};
+}
+
+void check_kkt(const b2p_kkt* k) {
+  if (!k) throw invalid("b2p: null kkt");
+  if (k->N < 0 || k->n < 1 || k->m < 0)
+    throw invalid("b2p_kkt: need N >= 0, n >= 1, m >= 0");
+  check_blocktri(k->N + 1, k->n);
+  if (k->m > 32) throw invalid("b2p: control dim > 32 is not supported");
+}
+
+// Formation (K1) for `B` systems whose inputs are at device view `kv`.
+template <class T>
+void launch_form(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, T* S, T* gamma, T* ti,
+                 int* errkey, cudaStream_t st) {
+  FormParams<T> f;
+  f.B = B;
+  f.N = k->N;
+  f.n = k->n;
+  f.m = k->m;
+  f.Q = static_cast<const T*>(kv.Q);
+  f.q = static_cast<const T*>(kv.q);
+  f.R = static_cast<const T*>(kv.R);
+  f.r = static_cast<const T*>(kv.r);
+  f.A = static_cast<const T*>(kv.A);
+  f.Bm = static_cast<const T*>(kv.B);
+  f.e = static_cast<const T*>(kv.e);
+  f.x_s = static_cast<const T*>(kv.x_s);
+  f.x0 = static_cast<const T*>(kv.x0);
+  f.S = S;
+  f.gamma = gamma;
+  f.theta_inv = ti;
+  f.errkey = errkey;
+  CK(cudaMemsetAsync(errkey, 0x7f, sizeof(int) * B, st));  // 0x7f7f7f7f: see below
+  CK(launch_build_schur<T>(f, st));
+  c->launches++;
+}
+// errkey is initialised with bytes 0x7f => 0x7f7f7f7f; the kernels treat any
+// value >= 0x7f7f7f7f as "ok". Normalise for the PCG kernel check:
+constexpr int kErrOk = 0x7f7f7f7f;
+
+// Fused batched solve on device data: K1 formation -> K3 PCG (fused mode).
+template <class T>
+void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, int kind,
+                       int order, const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
+                       SysOut* outs_dev, int* errkey, double* trace_dev, int trace_cap,
+                       cudaStream_t st, bool time_it, const std::string& tag) {
+  const int K = k->N + 1, n = k->n;
+  const size_t nn = static_cast<size_t>(n) * n, D = static_cast<size_t>(K) * n;
+  T* S = static_cast<T*>(ws_get(c, tag + "S", sizeof(T) * B * K * 3 * nn));
+  T* gamma = static_cast<T*>(ws_get(c, tag + "gamma", sizeof(T) * B * D));
+  T* ti = static_cast<T*>(ws_get(c, tag + "ti", sizeof(T) * B * K * nn));
+  if (time_it) {
+    if (!c->accounting) c->pool_used = 0;
+    if (c->pool_used + 3 > c->pool.size())
+      for (int q = 0; q < 3; ++q) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->pool.push_back(e);
+      }
+    c->ev0 = c->pool[c->pool_used];
+    c->ev2 = c->pool[c->pool_used + 1];
+    c->ev1 = c->pool[c->pool_used + 2];
+    c->pool_used += 3;
+    CK(cudaEventRecord(c->ev0, st));
+  }
+  launch_form<T>(c, k, kv, B, S, gamma, ti, errkey, st);
+  if (time_it) CK(cudaEventRecord(c->ev2, st));
+  c->phases = time_it;
+  PcgParams<T> p{};
+  p.B = B;
+  pcg_common(p, cfg, K, n);
+  p.kind = kind;
+  p.order = order;
+  p.mode = kModeFused;
+  p.S = S;
+  p.Phi = nullptr;
+  p.Tinv = ti;
+  p.gamma = gamma;
+  p.lambda0 = static_cast<const T*>(lambda0);
+  p.lambda_out = static_cast<T*>(lambda_out);
+  p.errkey = errkey;
+  p.out = outs_dev;
+  p.trace = trace_dev;
+  p.trace_cap = trace_cap;
+  configure_pcg(c, p, /*allow_grid=*/B == 1);
+  const size_t Dall = D * B;
+  p.best = static_cast<T*>(ws_get(c, tag + "best", sizeof(T) * Dall));
+  p.pub = static_cast<T*>(ws_get(c, tag + "pub", sizeof(T) * Dall));
+  p.slots = static_cast<T*>(ws_get(c, tag + "slots", sizeof(T) * 2 * p.G * B + 64));
+  CK(launch_pcg<T>(p, st));
+  c->launches++;
+  if (time_it) CK(cudaEventRecord(c->ev1, st));
+}
+
+void check_cfg(const b2p_pcg_config* cfg) {
+  if (cfg && cfg->variant != B2P_SEQUENTIAL && cfg->variant != B2P_BLOCK_PARALLEL)
+    throw invalid("b2p: unknown PCG variant");
+}
+void check_kind(int kind, int order) {
+  if (kind < B2P_IDENTITY || kind > B2P_POLY_SPLIT)
+    throw invalid("build_preconditioner: unknown kind");
+  if (kind == B2P_POLY_SPLIT && order < 1)
+    throw invalid("build_poly_split: order must be >= 1, got " + std::to_string(order));
+}
+
+// Resolve per-system outcomes (host copies) into reports and a first error.
+void resolve(const std::vector<SysOut>& outs, const std::vector<int>& errkeys, int B,
+             b2p_solve_report* reports, double wall_each, Fail* first) {
+  for (int i = 0; i < B; ++i) {
+    SysOut o = outs[i];
+    Fail f{B2P_OK, ""};
+    if (!errkeys.empty() && errkeys[i] < kErrOk) {
+      f.code = B2P_RUNTIME_ERROR;
+      f.msg = schur_msg(errkeys[i], &f.knot);
+      o = SysOut{};
+      o.code = B2P_RUNTIME_ERROR;
+    } else if (o.code != kOk) {
+      f = pcg_fail(o);
+    }
+    if (reports) fill_report(reports + i, o, wall_each);
+    if (f.code != B2P_OK && first->code == B2P_OK) {
+      *first = f;
+      first->system = i;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ generator
+// random_problem.cpp — host-side synthetic inputs (same draw order).
+struct Rng {
+  std::mt19937_64 g;
+  explicit Rng(uint64_t s) : g(s) {}
+  double u(double lo, double hi) {
+    const double u01 = static_cast<double>(g() >> 11) * 0x1.0p-53;
+    return lo + (hi - lo) * u01;
+  }
+  void mat(double* M, int r, int c, double lo, double hi) {
+    for (int i = 0; i < r * c; ++i) M[i] = u(lo, hi);
+  }
+};
+
+// Q = a * (L L') + floor*I  (p-ordered dot products)
+void llt(const double* L, int n, double* Q, double scale_prod, double diag, double outer) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int p = 0; p < n; ++p) s += L[i * n + p] * L[j * n + p];
+      double v = scale_prod * s;
+      if (i == j) v += diag;
+      Q[i * n + j] = outer * v;
+    }
+}
+
+void generate_one(int family, uint64_t seed, int N, int n, int m, double fl, double cp,
+                  b2p_kkt_out* o, size_t i) {
+  Rng rng(seed);
+  const size_t K = N + 1, nn = size_t(n) * n, mm = size_t(m) * m, nm = size_t(n) * m;
+  double* Q = o->Q + i * K * nn;
+  double* q = o->q + i * K * n;
+  double* R = o->R + i * N * mm;
+  double* r = o->r + i * N * m;
+  double* A = o->A + i * N * nn;
+  double* B = o->B + i * N * nm;
+  double* e = o->e + i * N * n;
+  std::vector<double> L(std::max(nn, mm));
+  const bool traj = family == 2;
+  const double cs = 2e-4;
+  for (int k = 0; k < N; ++k) {
+    rng.mat(L.data(), n, n, -1.0, 1.0);
+    if (traj) llt(L.data(), n, Q + k * nn, 0.3, 1.0, cs);
+    else llt(L.data(), n, Q + k * nn, 1.0, fl, 1.0);
+    rng.mat(L.data(), m, m, -1.0, 1.0);
+    if (traj) llt(L.data(), m, R + k * mm, 0.3, 1.0, cs);
+    else llt(L.data(), m, R + k * mm, 1.0, fl, 1.0);
+    double* Ak = A + k * nn;
+    rng.mat(Ak, n, n, -1.0, 1.0);
+    if (traj) {
+      for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+          Ak[a * n + b] = (a == b ? 0.1 : 0.0) + Ak[a * n + b] * (0.02 / n);
+    } else {
+      for (size_t a = 0; a < nn; ++a) Ak[a] *= (cp / n);
+    }
+    double* Bk = B + k * nm;
+    rng.mat(Bk, n, m, -1.0, 1.0);
+    for (size_t a = 0; a < nm; ++a) Bk[a] *= (traj ? 1.0 / n : cp / n);
+    rng.mat(q + k * n, 1, n, -1.0, 1.0);
+    rng.mat(r + k * m, 1, m, -1.0, 1.0);
+    rng.mat(e + k * n, 1, n, -1.0, 1.0);
+  }
+  rng.mat(L.data(), n, n, -1.0, 1.0);
+  if (traj) llt(L.data(), n, Q + N * nn, 0.3, 1.0, cs);
+  else llt(L.data(), n, Q + N * nn, 1.0, fl, 1.0);
+  rng.mat(q + N * n, 1, n, -1.0, 1.0);
+  rng.mat(o->x_s + i * n, 1, n, -1.0, 1.0);
+  for (int a = 0; a < n; ++a) o->x0[i * n + a] = 0.0;
+}
+
+}  // namespace
+
+// ======================================================================= C-ABI
+extern "C" {
+
+int b2p_abi_version(void) { return B2P_ABI_VERSION; }
+
+int b2p_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int b2p_ctx_create(int device, b2p_ctx** out, b2p_error* err) {
+  return guard(err, [&] {
+    if (!out) throw invalid("b2p_ctx_create: null out");
+    *out = nullptr;
+    int ndev = b2p_device_count();
+    if (ndev <= 0) throw Fail{B2P_CUDA_ERROR, "b2p: no CUDA device visible"};
+    if (device < 0 || device >= ndev) throw invalid("b2p_ctx_create: bad device index");
+    CK(cudaSetDevice(device));
+    auto* c = new b2p_ctx();
+    c->device = device;
+    CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    for (int q = 0; q < 3; ++q) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->pool.push_back(e);
+    }
+    c->ev0 = c->pool[0];
+    c->ev2 = c->pool[1];
+    c->ev1 = c->pool[2];
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    c->sm_count = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    *out = c;
+  });
+}
+
+void b2p_ctx_destroy(b2p_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->own);
+  cudaStreamSynchronize(c->aux);
+  for (auto& kv : c->ws)
+    if (kv.second.first) cudaFree(kv.second.first);
+  for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
+  cudaStreamDestroy(c->own);
+  cudaStreamDestroy(c->aux);
+  delete c;
+}
+
+int b2p_ctx_set_stream(b2p_ctx* c, void* stream) {
+  if (!c) return B2P_INVALID_ARGUMENT;
+  c->user = static_cast<cudaStream_t>(stream);
+  return B2P_OK;
+}
+void* b2p_ctx_stream(b2p_ctx* c) { return c ? static_cast<void*>(c->stream()) : nullptr; }
+long long b2p_ctx_kernel_launches(b2p_ctx* c) { return c ? c->launches.load() : 0; }
+int b2p_ctx_last_phase_ms(b2p_ctx* c, float* ms, int n) {
+  if (!c || !ms || n < 2) return B2P_INVALID_ARGUMENT;
+  ms[0] = ms[1] = 0.f;
+  if (!c->phases) return B2P_OK;
+  cudaSetDevice(c->device);
+  if (cudaEventElapsedTime(&ms[0], c->ev0, c->ev2) != cudaSuccess ||
+      cudaEventElapsedTime(&ms[1], c->ev2, c->ev1) != cudaSuccess) {
+    cudaGetLastError();
+    return B2P_CUDA_ERROR;
+  }
+  return B2P_OK;
+}
+
+int b2p_ctx_phase_accounting(b2p_ctx* c, int enable) {
+  if (!c) return B2P_INVALID_ARGUMENT;
+  c->accounting = enable != 0;
+  c->pool_used = 0;
+  return B2P_OK;
+}
+
+int b2p_ctx_phase_totals(b2p_ctx* c, float* ms, int n, int* count) {
+  if (!c || !ms || n < 3) return B2P_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  ms[0] = ms[1] = ms[2] = 0.f;
+  const size_t used = c->pool_used;
+  if (count) *count = static_cast<int>(used / 3);
+  for (size_t t = 0; t + 2 < used; t += 3) {
+    float a = 0.f, b = 0.f;
+    if (cudaEventSynchronize(c->pool[t + 2]) != cudaSuccess ||
+        cudaEventElapsedTime(&a, c->pool[t], c->pool[t + 1]) != cudaSuccess ||
+        cudaEventElapsedTime(&b, c->pool[t + 1], c->pool[t + 2]) != cudaSuccess) {
+      cudaGetLastError();
+      return B2P_CUDA_ERROR;
+    }
+    ms[0] += a;
+    ms[1] += b;
+    ms[2] += a + b;
+  }
+  c->pool_used = 0;
+  return B2P_OK;
+}
+
+int b2p_ctx_last_solve_ms(b2p_ctx* c, float* ms) {
+  if (!c || !ms) return B2P_INVALID_ARGUMENT;
+  *ms = c->last_ms;
+  return B2P_OK;
+}
+
+// ---------------------------------------------------------------- block_tri
+int b2p_blocktri_matvec(b2p_ctx* c, int dtype, int K, int nb, const void* M, const void* x,
+                        int x_len, void* y, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_blocktri(K, nb);
+    if (x_len != K * nb)
+      throw invalid("BlockTriMatrix matvec: expected vector of length " + std::to_string(K * nb) +
+                    ", got " + std::to_string(x_len));
+    check_ctx(c);
+    const size_t es = esize(dtype), nn = size_t(nb) * nb, D = size_t(K) * nb;
+    cudaStream_t st = c->stream();
+    char* dM = static_cast<char*>(ws_get(c, "mv_M", es * K * 3 * nn));
+    char* dx = static_cast<char*>(ws_get(c, "mv_x", es * D));
+    char* dy = static_cast<char*>(ws_get(c, "mv_y", es * D));
+    h2d(c, dM, M, es * K * 3 * nn, st);
+    h2d(c, dx, x, es * D, st);
+    if (dtype == B2P_F64)
+      CK(launch_blocktri_matvec<double>(1, K, nb, (double*)dM, (double*)dx, (double*)dy, 0,
+                                        nullptr, nullptr, st));
+    else
+      CK(launch_blocktri_matvec<float>(1, K, nb, (float*)dM, (float*)dx, (float*)dy, 0, nullptr,
+                                       nullptr, st));
+    c->launches++;
+    d2h(c, y, dy, es * D, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int b2p_blocktri_cholesky_solve(b2p_ctx* c, int dtype, int K, int nb, const void* M,
+                                const void* rhs, int rhs_len, void* x, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_blocktri(K, nb);
+    if (rhs_len != K * nb)
+      throw invalid("BlockTriMatrix cholesky_solve: expected vector of length " +
+                    std::to_string(K * nb) + ", got " + std::to_string(rhs_len));
+    check_ctx(c);
+    const size_t es = esize(dtype), nn = size_t(nb) * nb, D = size_t(K) * nb;
+    cudaStream_t st = c->stream();
+    char* dM = static_cast<char*>(ws_get(c, "ch_M", es * K * 3 * nn));
+    char* db = static_cast<char*>(ws_get(c, "ch_b", es * D));
+    char* dx = static_cast<char*>(ws_get(c, "ch_x", es * D));
+    char* dy = static_cast<char*>(ws_get(c, "ch_y", es * D));
+    char* dF = static_cast<char*>(ws_get(c, "ch_F", es * K * nn));
+    int* dst = static_cast<int*>(ws_get(c, "ch_st", sizeof(int)));
+    h2d(c, dM, M, es * K * 3 * nn, st);
+    h2d(c, db, rhs, es * D, st);
+    if (dtype == B2P_F64)
+      CK(launch_block_cholesky<double>(K, nb, (double*)dM, (double*)db, (double*)dx, (double*)dF,
+                                       (double*)dy, dst, st));
+    else
+      CK(launch_block_cholesky<float>(K, nb, (float*)dM, (float*)db, (float*)dx, (float*)dF,
+                                      (float*)dy, dst, st));
+    c->launches++;
+    int status = 0;
+    d2h(c, &status, dst, sizeof(int), st);
+    d2h(c, x, dx, es * D, st);
+    CK(cudaStreamSynchronize(st));
+    if (status >= 0)
+      throw Fail{B2P_RUNTIME_ERROR, "BlockTriMatrix cholesky_solve: block " +
+                                        std::to_string(status) + " is not positive definite"};
+  });
+}
+
+int b2p_blocktri_check(b2p_ctx* c, int dtype, int K, int nb, const void* M, double* asym,
+                       double* mabs, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_blocktri(K, nb);
+    check_ctx(c);
+    const size_t es = esize(dtype), nn = size_t(nb) * nb;
+    cudaStream_t st = c->stream();
+    char* dM = static_cast<char*>(ws_get(c, "ck_M", es * K * 3 * nn));
+    double* d2 = static_cast<double*>(ws_get(c, "ck_out", 2 * sizeof(double)));
+    h2d(c, dM, M, es * K * 3 * nn, st);
+    CK(cudaMemsetAsync(d2, 0, 2 * sizeof(double), st));
+    if (dtype == B2P_F64) CK(launch_blocktri_check<double>(K, nb, (double*)dM, d2, st));
+    else CK(launch_blocktri_check<float>(K, nb, (float*)dM, d2, st));
+    c->launches++;
+    double h[2];
+    d2h(c, h, d2, sizeof(h), st);
+    CK(cudaStreamSynchronize(st));
+    if (asym) *asym = h[0];
+    if (mabs) *mabs = h[1];
+  });
+}
+
+// ---------------------------------------------------------------- schur
+int b2p_build_schur(b2p_ctx* c, int dtype, const b2p_kkt* k, void* S, void* gamma,
+                    void* theta_inv, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(k);
+    check_ctx(c);
+    const size_t es = esize(dtype);
+    const int K = k->N + 1, n = k->n;
+    const size_t nn = size_t(n) * n, D = size_t(K) * n;
+    cudaStream_t st = c->stream();
+    void* in = ws_get(c, "bs_in", kkt_block_bytes(k, es, 1));
+    const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st);
+    char* dS = static_cast<char*>(ws_get(c, "bs_S", es * K * 3 * nn));
+    char* dg = static_cast<char*>(ws_get(c, "bs_g", es * D));
+    char* dt = static_cast<char*>(ws_get(c, "bs_t", es * K * nn));
+    int* ek = static_cast<int*>(ws_get(c, "bs_ek", sizeof(int)));
+    if (dtype == B2P_F64) launch_form<double>(c, k, kv, 1, (double*)dS, (double*)dg, (double*)dt, ek, st);
+    else launch_form<float>(c, k, kv, 1, (float*)dS, (float*)dg, (float*)dt, ek, st);
+    int key = 0;
+    d2h(c, &key, ek, sizeof(int), st);
+    d2h(c, S, dS, es * K * 3 * nn, st);
+    d2h(c, gamma, dg, es * D, st);
+    d2h(c, theta_inv, dt, es * K * nn, st);
+    CK(cudaStreamSynchronize(st));
+    if (key < kErrOk) {
+      Fail f{B2P_RUNTIME_ERROR, schur_msg(key, nullptr)};
+      schur_msg(key, &f.knot);
+      throw f;
+    }
+  });
+}
+
+int b2p_stair_matrix(b2p_ctx* c, int dtype, int K, int nb, const void* S, void* psi,
+                     b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_blocktri(K, nb);
+    check_ctx(c);
+    const size_t es = esize(dtype), bytes = es * K * 3 * size_t(nb) * nb;
+    cudaStream_t st = c->stream();
+    char* dS = static_cast<char*>(ws_get(c, "sm_S", bytes));
+    char* dP = static_cast<char*>(ws_get(c, "sm_P", bytes));
+    h2d(c, dS, S, bytes, st);
+    if (dtype == B2P_F64) CK(launch_stair_matrix<double>(K, nb, (double*)dS, (double*)dP, st));
+    else CK(launch_stair_matrix<float>(K, nb, (float*)dS, (float*)dP, st));
+    c->launches++;
+    d2h(c, psi, dP, bytes, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int b2p_build_preconditioner(b2p_ctx* c, int dtype, int kind, int order, int K, int nb,
+                             const void* S, const void* theta_inv, void* phi_inv,
+                             b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kind(kind, order);
+    if (kind == B2P_IDENTITY) return;  // build_identity: empty phi_inv
+    check_blocktri(K, nb);
+    check_ctx(c);
+    const size_t es = esize(dtype), nn = size_t(nb) * nb;
+    cudaStream_t st = c->stream();
+    char* dS = static_cast<char*>(ws_get(c, "bp_S", es * K * 3 * nn));
+    char* dt = static_cast<char*>(ws_get(c, "bp_t", es * K * nn));
+    char* dP = static_cast<char*>(ws_get(c, "bp_P", es * K * 3 * nn));
+    h2d(c, dS, S, es * K * 3 * nn, st);
+    h2d(c, dt, theta_inv, es * K * nn, st);
+    if (dtype == B2P_F64) {
+      PrecondParams<double> p{1, K, nb, kind, (double*)dS, (double*)dt, (double*)dP};
+      CK(launch_build_precond<double>(p, st));
+    } else {
+      PrecondParams<float> p{1, K, nb, kind, (float*)dS, (float*)dt, (float*)dP};
+      CK(launch_build_precond<float>(p, st));
+    }
+    c->launches++;
+    d2h(c, phi_inv, dP, es * K * 3 * nn, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int b2p_apply_preconditioner(b2p_ctx* c, int dtype, int kind, int order, int K, int nb,
+                             const void* S, const void* phi_inv, const void* r, int r_len,
+                             void* out, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kind(kind, order);
+    const size_t es = esize(dtype);
+    if (kind == B2P_IDENTITY) {  // returns r unchanged (schur.cpp:176-178)
+      std::memcpy(out, r, es * r_len);
+      return;
+    }
+    check_blocktri(K, nb);
+    if (r_len != K * nb)
+      throw invalid("apply_preconditioner: expected vector of length " + std::to_string(K * nb) +
+                    ", got " + std::to_string(r_len));
+    check_ctx(c);
+    const size_t nn = size_t(nb) * nb, D = size_t(K) * nb;
+    cudaStream_t st = c->stream();
+    char* dP = static_cast<char*>(ws_get(c, "ap_P", es * K * 3 * nn));
+    char* dr = static_cast<char*>(ws_get(c, "ap_r", es * D));
+    char* dacc = static_cast<char*>(ws_get(c, "ap_acc", es * D));
+    h2d(c, dP, phi_inv, es * K * 3 * nn, st);
+    h2d(c, dr, r, es * D, st);
+    auto mv = [&](const void* M, const void* x, void* y, int mode, const void* add, void* acc) {
+      if (dtype == B2P_F64)
+        CK(launch_blocktri_matvec<double>(1, K, nb, (const double*)M, (const double*)x,
+                                          (double*)y, mode, (const double*)add, (double*)acc, st));
+      else
+        CK(launch_blocktri_matvec<float>(1, K, nb, (const float*)M, (const float*)x, (float*)y,
+                                         mode, (const float*)add, (float*)acc, st));
+      c->launches++;
+    };
+    if (kind != B2P_POLY_SPLIT) {
+      mv(dP, dr, dacc, 0, nullptr, nullptr);
+    } else {
+      char* dS = static_cast<char*>(ws_get(c, "ap_S", es * K * 3 * nn));
+      char* dterm = static_cast<char*>(ws_get(c, "ap_term", es * D));
+      char* ds = static_cast<char*>(ws_get(c, "ap_s", es * D));
+      char* dacc2 = static_cast<char*>(ws_get(c, "ap_acc2", es * D));
+      h2d(c, dS, S, es * K * 3 * nn, st);
+      mv(dP, dr, dterm, 0, nullptr, nullptr);  // term = Phi r
+      CK(cudaMemcpyAsync(dacc, dterm, es * D, cudaMemcpyDeviceToDevice, st));
+      for (int j = 0; j < order; ++j) {
+        mv(dS, dterm, ds, 1, nullptr, nullptr);  // s = E term
+        mv(dP, ds, dterm, 0, dacc, dacc2);       // term = Phi s; acc2 = acc + term
+        std::swap(dacc, dacc2);
+      }
+    }
+    d2h(c, out, dacc, es * D, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+// ---------------------------------------------------------------- pcg
+int b2p_pcg_solve(b2p_ctx* c, int dtype, int K, int nb, const void* S, int kind, int order,
+                  int phi_K, int phi_nb, const void* phi_inv, const void* gamma, int gamma_len,
+                  const void* lambda0, int lambda0_len, const b2p_pcg_config* cfg,
+                  void* lambda_out, b2p_solve_report* report, double* trace, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_cfg(cfg);
+    // validate_inputs (pcg.cpp:24-47)
+    if (K <= 0) throw invalid("pcg: empty system matrix");
+    const int dim = K * nb;
+    if (gamma_len != dim)
+      throw invalid("pcg: expected gamma of length " + std::to_string(dim) + ", got " +
+                    std::to_string(gamma_len));
+    if (lambda0_len != dim)
+      throw invalid("pcg: expected lambda0 of length " + std::to_string(dim) + ", got " +
+                    std::to_string(lambda0_len));
+    check_kind(kind, order);
+    if (kind != B2P_IDENTITY && phi_K * phi_nb != dim)
+      throw invalid("pcg: preconditioner dimension " + std::to_string(phi_K * phi_nb) +
+                    " does not match system " + std::to_string(dim));
+    if (kind != B2P_IDENTITY && phi_nb != nb)
+      throw invalid("b2p: preconditioner block_dim must match S");
+    check_blocktri(K, nb);
+    check_ctx(c);
+    const size_t es = esize(dtype), nn = size_t(nb) * nb, D = size_t(dim);
+    cudaStream_t st = c->stream();
+    char* dS = static_cast<char*>(ws_get(c, "pc_S", es * K * 3 * nn));
+    char* dP = kind != B2P_IDENTITY ? static_cast<char*>(ws_get(c, "pc_P", es * K * 3 * nn))
+                                    : nullptr;
+    char* dg = static_cast<char*>(ws_get(c, "pc_g", es * D));
+    char* dl0 = static_cast<char*>(ws_get(c, "pc_l0", es * D));
+    char* dl = static_cast<char*>(ws_get(c, "pc_l", es * D));
+    SysOut* dout = static_cast<SysOut*>(ws_get(c, "pc_out", sizeof(SysOut)));
+    h2d(c, dS, S, es * K * 3 * nn, st);
+    if (dP) h2d(c, dP, phi_inv, es * K * 3 * nn, st);
+    h2d(c, dg, gamma, es * D, st);
+    h2d(c, dl0, lambda0, es * D, st);
+    // asymmetry check on device (validate_inputs :42-46)
+    double* d2 = static_cast<double*>(ws_get(c, "pc_ck", 2 * sizeof(double)));
+    CK(cudaMemsetAsync(d2, 0, 2 * sizeof(double), st));
+    if (dtype == B2P_F64) CK(launch_blocktri_check<double>(K, nb, (double*)dS, d2, st));
+    else CK(launch_blocktri_check<float>(K, nb, (float*)dS, d2, st));
+    c->launches++;
+    double ck[2];
+    d2h(c, ck, d2, sizeof(ck), st);
+    CK(cudaStreamSynchronize(st));
+    if (ck[0] > 1e-9 * std::max(1.0, ck[1]))
+      throw invalid("pcg: S is not structurally symmetric (asymmetry " + fstr(ck[0]) + ")");
+    int trace_cap = 0;
+    double* dtr = nullptr;
+    const int mi = (cfg && cfg->max_iter > 0) ? cfg->max_iter : dim;
+    if (trace && cfg && cfg->collect_trace) {
+      trace_cap = mi;
+      dtr = static_cast<double*>(ws_get(c, "pc_tr", sizeof(double) * trace_cap));
+    }
+    auto go = [&](auto tag) {
+      using T = decltype(tag);
+      PcgParams<T> p{};
+      p.B = 1;
+      pcg_common(p, cfg, K, nb);
+      p.kind = kind;
+      p.order = order;
+      p.mode = kModeExplicit;
+      p.S = (const T*)dS;
+      p.Phi = (const T*)dP;
+      p.Tinv = nullptr;
+      p.gamma = (const T*)dg;
+      p.lambda0 = (const T*)dl0;
+      p.lambda_out = (T*)dl;
+      p.errkey = nullptr;
+      p.out = dout;
+      p.trace = dtr;
+      p.trace_cap = trace_cap;
+      configure_pcg(c, p, true);
+      run_pcg<T>(c, p, st, true);
+    };
+    if (dtype == B2P_F64) go(double{});
+    else go(float{});
+    SysOut o;
+    d2h(c, &o, dout, sizeof(SysOut), st);
+    d2h(c, lambda_out, dl, es * D, st);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    if (o.code != kOk) throw pcg_fail(o);
+    if (dtr && o.trace_len > 0) CK(cudaMemcpy(trace, dtr, sizeof(double) * o.trace_len,
+                                             cudaMemcpyDeviceToHost));
+    fill_report(report, o, c->last_ms * 1e-3);
+  });
+}
+
+// ---------------------------------------------------------------- fused
+int b2p_solve(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
+              const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
+              b2p_solve_report* report, double* trace, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(k);
+    check_kind(kind, order);
+    check_cfg(cfg);
+    check_ctx(c);
+    const size_t es = esize(dtype);
+    const int K = k->N + 1, n = k->n;
+    const size_t D = size_t(K) * n;
+    cudaStream_t st = c->stream();
+    void* in = ws_get(c, "sv_in", kkt_block_bytes(k, es, 1));
+    const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st);
+    char* dl0 = nullptr;
+    if (lambda0) {
+      dl0 = static_cast<char*>(ws_get(c, "sv_l0", es * D));
+      h2d(c, dl0, lambda0, es * D, st);
+    }
+    char* dl = static_cast<char*>(ws_get(c, "sv_l", es * D));
+    SysOut* dout = static_cast<SysOut*>(ws_get(c, "sv_out", sizeof(SysOut)));
+    int* ek = static_cast<int*>(ws_get(c, "sv_ek", sizeof(int)));
+    const int mi = (cfg && cfg->max_iter > 0) ? cfg->max_iter : int(D);
+    double* dtr = nullptr;
+    if (trace && cfg && cfg->collect_trace)
+      dtr = static_cast<double*>(ws_get(c, "sv_tr", sizeof(double) * mi));
+    if (dtype == B2P_F64)
+      solve_device_impl<double>(c, k, kv, 1, kind, order, cfg, dl0, dl, dout, ek, dtr, mi, st,
+                                true, "sv_");
+    else
+      solve_device_impl<float>(c, k, kv, 1, kind, order, cfg, dl0, dl, dout, ek, dtr, mi, st,
+                               true, "sv_");
+    SysOut o;
+    int key = 0;
+    d2h(c, &o, dout, sizeof(o), st);
+    d2h(c, &key, ek, sizeof(int), st);
+    d2h(c, lambda_out, dl, es * D, st);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    Fail first{B2P_OK, ""};
+    resolve({o}, {key}, 1, report, c->last_ms * 1e-3, &first);
+    if (first.code != B2P_OK) {
+      first.system = -1;
+      throw first;
+    }
+    if (dtr && o.trace_len > 0)
+      CK(cudaMemcpy(trace, dtr, sizeof(double) * o.trace_len, cudaMemcpyDeviceToHost));
+  });
+}
+
+int b2p_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd, int kind,
+                             int order, const b2p_pcg_config* cfg, const void* lambda0_dev,
+                             void* lambda_out_dev, b2p_solve_report* reports, int32_t* status_dev,
+                             b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(kd);
+    check_kind(kind, order);
+    check_cfg(cfg);
+    check_ctx(c);
+    if (batch < 1) throw invalid("b2p_solve_batched: batch must be >= 1");
+    cudaStream_t st = c->stream();
+    SysOut* dout = static_cast<SysOut*>(ws_get(c, "bd_out", sizeof(SysOut) * batch));
+    int* ek = static_cast<int*>(ws_get(c, "bd_ek", sizeof(int) * batch));
+    const KktDev kv = dev_view(kd);
+    if (dtype == B2P_F64)
+      solve_device_impl<double>(c, kd, kv, batch, kind, order, cfg, lambda0_dev, lambda_out_dev,
+                                dout, ek, nullptr, 0, st, true, "bd_");
+    else
+      solve_device_impl<float>(c, kd, kv, batch, kind, order, cfg, lambda0_dev, lambda_out_dev,
+                               dout, ek, nullptr, 0, st, true, "bd_");
+    (void)status_dev;
+    if (reports) {
+      std::vector<SysOut> outs(batch);
+      std::vector<int> keys(batch);
+      d2h(c, outs.data(), dout, sizeof(SysOut) * batch, st);
+      d2h(c, keys.data(), ek, sizeof(int) * batch, st);
+      CK(cudaStreamSynchronize(st));
+      CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+      Fail first{B2P_OK, ""};
+      resolve(outs, keys, batch, reports, c->last_ms * 1e-3 / batch, &first);
+      if (first.code != B2P_OK) throw first;
+    }
+  });
+}
+
+// Host-buffer batched solve: chunks of systems alternate between two
+// streams so the H2D copy of chunk c+1 overlaps the kernels of chunk c.
+int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int kind, int order,
+                      const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
+                      b2p_solve_report* reports, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(k);
+    check_kind(kind, order);
+    check_cfg(cfg);
+    check_ctx(c);
+    if (batch < 1) throw invalid("b2p_solve_batched: batch must be >= 1");
+    const size_t es = esize(dtype);
+    const int K = k->N + 1, n = k->n;
+    const size_t D = size_t(K) * n;
+    const int chunk = std::min(batch, std::max(1, env_int("B2P_BATCH_CHUNK", 1024)));
+    const int nchunks = (batch + chunk - 1) / chunk;
+    cudaStream_t streams[2] = {c->stream(), c->aux};
+    std::vector<SysOut> outs(batch);
+    std::vector<int> keys(batch);
+    cudaEvent_t start = nullptr, stop = nullptr;
+    CK(cudaEventCreate(&start));
+    CK(cudaEventCreate(&stop));
+    CK(cudaEventRecord(start, streams[0]));
+    CK(cudaStreamWaitEvent(streams[1], start, 0));
+    for (int ci = 0; ci < nchunks; ++ci) {
+      const int first = ci * chunk, cnt = std::min(chunk, batch - first);
+      const int sidx = ci & 1;
+      cudaStream_t st = streams[sidx];
+      const std::string tag = std::string("bh") + char('0' + sidx) + "_";
+      void* in = ws_get(c, tag + "in", kkt_block_bytes(k, es, chunk));
+      const KktDev kv = upload_kkt(c, k, es, first, cnt, in, st);
+      char* dl0 = nullptr;
+      if (lambda0) {
+        dl0 = static_cast<char*>(ws_get(c, tag + "l0", es * D * chunk));
+        h2d(c, dl0, static_cast<const char*>(lambda0) + es * D * first, es * D * cnt, st);
+      }
+      char* dl = static_cast<char*>(ws_get(c, tag + "l", es * D * chunk));
+      SysOut* dout = static_cast<SysOut*>(ws_get(c, tag + "out", sizeof(SysOut) * chunk));
+      int* ek = static_cast<int*>(ws_get(c, tag + "ek", sizeof(int) * chunk));
+      b2p_kkt kc = *k;
+      if (dtype == B2P_F64)
+        solve_device_impl<double>(c, &kc, kv, cnt, kind, order, cfg, dl0, dl, dout, ek, nullptr,
+                                  0, st, false, tag);
+      else
+        solve_device_impl<float>(c, &kc, kv, cnt, kind, order, cfg, dl0, dl, dout, ek, nullptr, 0,
+                                 st, false, tag);
+      d2h(c, static_cast<char*>(lambda_out) + es * D * first, dl, es * D * cnt, st);
+      d2h(c, outs.data() + first, dout, sizeof(SysOut) * cnt, st);
+      d2h(c, keys.data() + first, ek, sizeof(int) * cnt, st);
+    }
+    cudaEvent_t join = nullptr;
+    CK(cudaEventCreate(&join));
+    CK(cudaEventRecord(join, streams[1]));
+    CK(cudaStreamWaitEvent(streams[0], join, 0));
+    CK(cudaEventRecord(stop, streams[0]));
+    CK(cudaEventSynchronize(stop));
+    CK(cudaEventElapsedTime(&c->last_ms, start, stop));
+    cudaEventDestroy(start);
+    cudaEventDestroy(stop);
+    cudaEventDestroy(join);
+    Fail firstf{B2P_OK, ""};
+    resolve(outs, keys, batch, reports, c->last_ms * 1e-3 / batch, &firstf);
+    if (firstf.code != B2P_OK) throw firstf;
+  });
+}
+
+int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
+                            const b2p_kkt* k, int kind, int order, const b2p_pcg_config* cfg,
+                            const void* lambda0, void* lambda_out, b2p_solve_report* reports,
+                            b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(k);
+    if (!devices || ndev < 1) throw invalid("b2p_solve_batched_multi: need >= 1 device");
+    const size_t es = esize(dtype);
+    const int K = k->N + 1, n = k->n, m = k->m, N = k->N;
+    const size_t D = size_t(K) * n;
+    std::vector<int> rc(ndev, B2P_OK);
+    std::vector<b2p_error> errs(ndev);
+    std::vector<std::thread> th;
+    const int per = (batch + ndev - 1) / ndev;
+    for (int g = 0; g < ndev; ++g) {
+      th.emplace_back([&, g] {
+        const int first = g * per, cnt = std::min(per, batch - first);
+        if (cnt <= 0) return;
+        b2p_ctx* cx = nullptr;
+        rc[g] = b2p_ctx_create(devices[g], &cx, &errs[g]);
+        if (rc[g] != B2P_OK) return;
+        // contiguous batch-index shard
+        const size_t nn = size_t(n) * n, Kz = K, Nz = N;
+        auto off = [&](const void* p, size_t per_sys) {
+          return static_cast<const void*>(static_cast<const char*>(p) + es * per_sys * first);
+        };
+        b2p_kkt s = *k;
+        s.Q = off(k->Q, Kz * nn);
+        s.q = off(k->q, Kz * n);
+        s.R = off(k->R, Nz * m * m);
+        s.r = off(k->r, Nz * m);
+        s.A = off(k->A, Nz * nn);
+        s.B = off(k->B, Nz * n * m);
+        s.e = off(k->e, Nz * n);
+        s.x_s = off(k->x_s, n);
+        s.x0 = off(k->x0, n);
+        const void* l0 = lambda0 ? static_cast<const char*>(lambda0) + es * D * first : nullptr;
+        void* lo = static_cast<char*>(lambda_out) + es * D * first;
+        rc[g] = b2p_solve_batched(cx, dtype, cnt, &s, kind, order, cfg, l0, lo,
+                                  reports ? reports + first : nullptr, &errs[g]);
+        if (rc[g] != B2P_OK) errs[g].system += first;
+        b2p_ctx_destroy(cx);
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int g = 0; g < ndev; ++g)
+      if (rc[g] != B2P_OK) {
+        Fail f{rc[g], errs[g].message};
+        f.knot = errs[g].knot;
+        f.iteration = errs[g].iteration;
+        f.system = errs[g].system;
+        throw f;
+      }
+  });
+}
+
+// ---------------------------------------------------------------- generator
+int b2p_random_kkt(int family, uint64_t seed, int N, int n, int m, double fl, double cp,
+                   b2p_kkt_out* out, b2p_error* err) {
+  return guard(err, [&] {
+    if (!out || N < 0 || n < 1 || m < 0) throw invalid("b2p_random_kkt: bad arguments");
+    generate_one(family, seed, N, n, m, fl, cp, out, 0);
+  });
+}
+
+int b2p_random_kkt_batch(int family, uint64_t seed0, int batch, int N, int n, int m, double fl,
+                         double cp, int threads, b2p_kkt_out* out, b2p_error* err) {
+  return guard(err, [&] {
+    if (!out || N < 0 || n < 1 || m < 0 || batch < 0)
+      throw invalid("b2p_random_kkt_batch: bad arguments");
+    int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+    T = std::max(1, std::min(T, batch));
+    std::vector<std::thread> th;
+    std::atomic<int> next{0};
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&] {
+        for (int i = next++; i < batch; i = next++)
+          generate_one(family, seed0 + static_cast<uint64_t>(i), N, n, m, fl, cp, out, i);
+      });
+    for (auto& t : th) t.join();
+  });
+}
+
+void* b2p_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+void b2p_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

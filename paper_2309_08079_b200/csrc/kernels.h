@@ -1,0 +1,82 @@
+// Kernel parameter blocks and launchers (host <-> device boundary inside the
+// library; the public C-ABI is include/b2p.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace b2p {
+
+template <class T>
+struct FormParams {
+  int B, N, n, m;
+  const T *Q, *q, *R, *r, *A, *Bm, *e, *x_s, *x0;  // [B][...] contiguous (b2p_kkt layout)
+  T* S;          // [B][K][3][n][n]
+  T* gamma;      // [B][K*n]
+  T* theta_inv;  // [B][K][n][n]
+  int* errkey;   // [B], INT_MAX = ok; else row*4 + call (see k_build_schur)
+};
+
+template <class T>
+struct PrecondParams {
+  int B, K, nb, kind;
+  const T* S;
+  const T* theta_inv;
+  T* phi;
+};
+
+enum : int { kModeExplicit = 0, kModeFused = 1 };
+enum : int { kSyncCta = 0, kSyncCluster = 1, kSyncGrid = 2 };
+
+template <class T>
+struct PcgParams {
+  int B, K, nb;
+  int G;         // CTAs per system
+  int rows_per;  // block rows owned per CTA
+  int kind, order;
+  int mode;   // kModeExplicit (user Phi) | kModeFused (theta_inv, Phi applied on the fly)
+  int stage;  // 1: copy the CTA's matrix rows into shared memory once
+  int sync;   // kSyncCta | kSyncCluster | kSyncGrid
+  int nthreads;
+  const T* S;        // [B][K][3][nb][nb]
+  const T* Phi;      // explicit: [B][K][3][nb][nb]
+  const T* Tinv;     // fused: [B][K][nb][nb]
+  const T* gamma;    // [B][D]
+  const T* lambda0;  // [B][D] or null (=> 0)
+  T* lambda_out;     // [B][D]
+  T* best;           // workspace [B][D]
+  T* pub;            // workspace [B][D]  (p exchange between CTAs)
+  T* slots;          // workspace [B][2][G]
+  const int* errkey; // [B] formation status or null
+  SysOut* out;       // [B]
+  double* trace;     // [B][trace_cap] or null
+  int trace_cap;
+  double epsilon;
+  int max_iter;
+  int check_drift;
+};
+
+// Shared-memory footprint of one PCG CTA (bytes) for a parameter block.
+template <class T>
+size_t pcg_smem_bytes(const PcgParams<T>& p);
+int pcg_halo(int kind, int order);
+
+template <class T> cudaError_t launch_build_schur(const FormParams<T>& p, cudaStream_t st);
+template <class T> cudaError_t launch_build_precond(const PrecondParams<T>& p, cudaStream_t st);
+template <class T>
+cudaError_t launch_blocktri_matvec(int B, int K, int nb, const T* M, const T* x, T* y, int mode,
+                                   const T* add_to, T* acc, cudaStream_t st);
+template <class T>
+cudaError_t launch_stair_matrix(int K, int nb, const T* S, T* psi, cudaStream_t st);
+template <class T>
+cudaError_t launch_blocktri_check(int K, int nb, const T* M, double* out2, cudaStream_t st);
+template <class T>
+cudaError_t launch_block_cholesky(int K, int nb, const T* M, const T* rhs, T* x, T* factors, T* y,
+                                  int* status, cudaStream_t st);
+template <class T> cudaError_t launch_pcg(const PcgParams<T>& p, cudaStream_t st);
+
+}  // namespace b2p
