@@ -341,9 +341,17 @@ def run_b200(a, world, rank, local):
     hbm, peak_src = peaks()
     k1_avg = k1_ms / max(1, nsolves)
     k3_avg = k3_ms / max(1, nsolves)
-    dom = "K3_pcg" if k3_avg >= k1_avg else "K1_schur_formation"
-    dom_ms = max(k1_avg, k3_avg)
-    dom_bytes = B * (alg["b_k3"] if dom == "K3_pcg" else alg["b_k1"])
+    fused = ctx.last_path() == 1
+    if fused:
+        # one persistent launch does K1+K2+K3: its compulsory HBM bytes are the
+        # KKT inputs in and lambda out (the L/D/theta^-1 staging stays in L2)
+        dom = "K13_fused"
+        dom_ms = k1_avg + k3_avg
+        dom_bytes = B * (alg["b_in"] + (N + 1) * n * 8)
+    else:
+        dom = "K3_pcg" if k3_avg >= k1_avg else "K1_schur_formation"
+        dom_ms = max(k1_avg, k3_avg)
+        dom_bytes = B * (alg["b_k3"] if dom == "K3_pcg" else alg["b_k1"])
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
@@ -366,7 +374,8 @@ def run_b200(a, world, rank, local):
                      "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "peak_source": peak_src,
                      "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
-                     "phase_ms_per_step": {"K1_schur_formation": k1_avg, "K3_pcg": k3_avg},
+                     "phase_ms_per_step": ({"K13_fused": k1_avg + k3_avg} if fused else
+                                           {"K1_schur_formation": k1_avg, "K3_pcg": k3_avg}),
                      "fp64_tflops_step": flops_step / (elapsed_ms / a.steps * 1e-3) / 1e12,
                      "b_full_GBs": B * alg["b_full"] / (elapsed_ms / a.steps * 1e-3) / 1e9},
         "pcg_iters": {"mean": mean_iters, "min": int(min(iters)), "max": int(max(iters))},

@@ -132,6 +132,9 @@ int b2p_ctx_set_stream(b2p_ctx* ctx, void* stream);
 void* b2p_ctx_stream(b2p_ctx* ctx);
 /* Number of kernels this context launched since creation (evidence counter). */
 long long b2p_ctx_kernel_launches(b2p_ctx* ctx);
+/* Which device path the most recent fused solve took: 1 = the persistent
+ * one-CTA-per-system K1+K3 kernel, 0 = split K1 formation + K3 PCG. */
+int b2p_ctx_last_path(b2p_ctx* ctx);
 
 /* ---- block_tri.hpp ---------------------------------------------------- */
 /* BlockTriMatrix::matvec (block_tri.cpp:70-92). */

@@ -42,6 +42,10 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self._lib.b2p_ctx_kernel_launches(self.handle))
 
+    def last_path(self) -> int:
+        """1 if the last fused solve ran the persistent K1+K3 kernel, 0 if split."""
+        return int(self._lib.b2p_ctx_last_path(self.handle))
+
     def last_solve_ms(self) -> float:
         v = C.c_float()
         self._lib.b2p_ctx_last_solve_ms(self.handle, C.byref(v))

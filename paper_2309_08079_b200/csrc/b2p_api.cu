@@ -37,6 +37,7 @@ struct b2p_ctx {
   std::vector<cudaEvent_t> pool;
   size_t pool_used = 0;
   float last_ms = 0.f;
+  int last_path = 0;  // 1: the fused persistent K1+K3 kernel ran
   std::atomic<long long> launches{0};
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
@@ -352,6 +353,56 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
                        cudaStream_t st, bool time_it, const std::string& tag) {
   const int K = k->N + 1, n = k->n;
   const size_t nn = static_cast<size_t>(n) * n, D = static_cast<size_t>(K) * n;
+  const bool drift = cfg && cfg->check_residual_drift && cfg->variant == B2P_SEQUENTIAL;
+  if (!drift && env_int("B2P_FUSED", 1) && fused_supported<T>(K, n, k->m, kind)) {
+    // persistent one-CTA-per-system K1+K3 kernel (fused_kernels.cu)
+    const int grid = std::max(1, std::min(B, c->sm_count));
+    FusedParams<T> f{};
+    f.B = B;
+    f.K = K;
+    f.kind = kind;
+    f.Q = static_cast<const T*>(kv.Q);
+    f.q = static_cast<const T*>(kv.q);
+    f.R = static_cast<const T*>(kv.R);
+    f.r = static_cast<const T*>(kv.r);
+    f.A = static_cast<const T*>(kv.A);
+    f.Bm = static_cast<const T*>(kv.B);
+    f.e = static_cast<const T*>(kv.e);
+    f.x_s = static_cast<const T*>(kv.x_s);
+    f.x0 = static_cast<const T*>(kv.x0);
+    f.slot = static_cast<T*>(ws_get(c, "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n)));
+    f.lambda0 = static_cast<const T*>(lambda0);
+    f.lambda_out = static_cast<T*>(lambda_out);
+    f.errkey = errkey;
+    f.out = outs_dev;
+    f.trace = trace_dev;
+    f.trace_cap = trace_cap;
+    f.epsilon = cfg ? cfg->epsilon : 1e-4;
+    const int mi = cfg ? cfg->max_iter : 0;
+    f.max_iter = mi > 0 ? mi : static_cast<int>(D);
+    if (time_it) {
+      if (!c->accounting) c->pool_used = 0;
+      if (c->pool_used + 3 > c->pool.size())
+        for (int q = 0; q < 3; ++q) {
+          cudaEvent_t e;
+          CK(cudaEventCreate(&e));
+          c->pool.push_back(e);
+        }
+      c->ev0 = c->pool[c->pool_used];
+      c->ev2 = c->pool[c->pool_used + 1];
+      c->ev1 = c->pool[c->pool_used + 2];
+      c->pool_used += 3;
+      CK(cudaEventRecord(c->ev0, st));
+      CK(cudaEventRecord(c->ev2, st));  // no separate formation launch
+    }
+    CK(launch_fused<T>(f, grid, st));
+    c->launches++;
+    c->last_path = 1;
+    c->phases = time_it;
+    if (time_it) CK(cudaEventRecord(c->ev1, st));
+    return;
+  }
+  c->last_path = 0;
   T* S = static_cast<T*>(ws_get(c, tag + "S", sizeof(T) * B * K * 3 * nn));
   T* gamma = static_cast<T*>(ws_get(c, tag + "gamma", sizeof(T) * B * D));
   T* ti = static_cast<T*>(ws_get(c, tag + "ti", sizeof(T) * B * K * nn));
@@ -566,6 +617,7 @@ int b2p_ctx_set_stream(b2p_ctx* c, void* stream) {
 }
 void* b2p_ctx_stream(b2p_ctx* c) { return c ? static_cast<void*>(c->stream()) : nullptr; }
 long long b2p_ctx_kernel_launches(b2p_ctx* c) { return c ? c->launches.load() : 0; }
+int b2p_ctx_last_path(b2p_ctx* c) { return c ? c->last_path : -1; }
 int b2p_ctx_last_phase_ms(b2p_ctx* c, float* ms, int n) {
   if (!c || !ms || n < 2) return B2P_INVALID_ARGUMENT;
   ms[0] = ms[1] = 0.f;

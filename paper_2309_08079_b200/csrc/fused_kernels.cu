@@ -1,0 +1,706 @@
+// K1+K2+K3 fused — persistent "one CTA per system" symmetric-stair PCG for
+// systems that fit one SM (c1: K=32, c4: K=64 at n=14, m=7, fp64).
+//
+// One launch solves a whole batch: gridDim.x CTAs (one per SM) loop over the
+// systems of the batch. Per system:
+//   F  (build_schur + preconditioner data, schur.cpp:38-82,109-142): each
+//      16-lane half-warp owns block rows h, h+32 (the rows it will own in the
+//      PCG phase) and computes, with compile-time n, m:
+//        Q_{k+1}^-1, R_k^-1, Q_k^-1  (Cholesky + triangular inverse, lane j
+//        holds column j in registers; symmetrised through a shared tile),
+//        L_b = -A Q_k^-1, D_b = theta_b = sym((A Q_k^-1) A' + (B R_k^-1) B'
+//        + Q_{k+1}^-1), gamma_b and theta_b^-1.
+//      L, D and theta^-1 go to a CTA-private global slot (L2 resident: the
+//      CTA rewrites the same 300 KB for every system), gamma stays in registers.
+//   P  (pcg_solve, pcg.cpp:55-129): L and D are copied into shared memory
+//      (row-major n x n blocks, read as 16-byte pairs along rows — conflict
+//      free for n = 14 — and as 8-byte columns for the R_b = L_{b+1}' product),
+//      theta^-1 rows live in registers of the thread that owns the row. The
+//      stair family is applied on the fly:
+//        t_j = theta_j^-1 r_j,  u_i = r_i - L_i t_{i-1} - R_i t_{i+1},
+//        r~_i = theta_i^-1 u_i   (odd rows for stair, all rows for symstair),
+//      the reference's materialised -theta_i^-1 L_i theta_{i-1}^-1 blocks
+//      re-associated (bitwise-symmetric S and theta^-1 make the symmetric-stair
+//      mirror exactly this formula on the even rows).
+//      upsilon and eta' are warp-shuffle trees + a fixed-order combine of the
+//      16 warp partials: bit-reproducible, no atomics.
+#include "kernels.h"
+
+namespace b2p {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kThreads = 512;  // 32 half-warps
+constexpr int kHalfWarps = kThreads / 16;
+
+template <int N>
+struct Odd {
+  static constexpr int v = N | 1;
+};
+
+// ---------------------------------------------------------------- half-warp dense helpers
+// Each 16-lane half-warp runs these independently (the two half-warps of a
+// warp may take different branches, e.g. block row 0 vs row 1), so every
+// shuffle / __syncwarp uses the half-warp's own lane mask. Lanes l >= N
+// compute on clamped data and never store.
+__device__ __forceinline__ unsigned hw_mask() {
+  return 0xffffu << (threadIdx.x & 16);
+}
+
+// In-place lower Cholesky of an N x N tile (stride LD, lower triangle read),
+// left-looking like Eigen's llt_inplace::unblocked. Returns the first failing
+// pivot (x <= 0; a NaN pivot passes, as in Eigen) or -1.
+template <class T, int N, int LD>
+__device__ __forceinline__ int hw_cholesky(T* A, T* rd, int l) {
+  // In-place lower Cholesky of an N x N tile (stride LD, lower triangle read),
+  // left-looking like Eigen's llt_inplace::unblocked; rd[k] = 1 / L(k,k).
+  // Returns the first failing pivot (x <= 0; a NaN pivot passes, as in Eigen)
+  // or -1. Divisions are replaced by one reciprocal per pivot.
+  int fail = -1;
+  const int lr = l < N ? l : N - 1;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    T s = A[lr * LD + k];
+#pragma unroll
+    for (int p = 0; p < k; ++p) s -= A[lr * LD + p] * A[k * LD + p];
+    T x = __shfl_sync(hw_mask(), s, k, 16);
+    if (x <= T(0)) {
+      if (fail < 0) fail = k;
+      x = T(1);
+    }
+    const T d = sqrt(x);
+    const T r = T(1) / d;
+    __syncwarp(hw_mask());
+    if (l == k) {
+      A[k * LD + k] = d;
+      rd[k] = r;
+    } else if (l > k && l < N) {
+      A[l * LD + k] = s * r;
+    }
+    __syncwarp(hw_mask());
+  }
+  return fail;
+}
+
+// x = column j of (L L')^{-1} (forward then backward substitution against e_j).
+template <class T, int N, int LD>
+__device__ __forceinline__ void hw_inv_col(const T* L, const T* rd, int j, T (&x)[N]) {
+  // __syncwarp between rows stops the scheduler from hoisting all N^2/2
+  // tile loads ahead of the recurrence (register blow-up / spills).
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T s = (i == j) ? T(1) : T(0);
+#pragma unroll
+    for (int p = 0; p < i; ++p) s -= L[i * LD + p] * x[p];
+    x[i] = s * rd[i];
+    __syncwarp(hw_mask());
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    T s = x[i];
+#pragma unroll
+    for (int p = i + 1; p < N; ++p) s -= L[p * LD + i] * x[p];
+    x[i] = s * rd[i];
+    __syncwarp(hw_mask());
+  }
+}
+
+// column j of X -> column j of 0.5 (X + X') through the tile W (overwritten).
+template <class T, int N, int LD>
+__device__ __forceinline__ void hw_symmetrize_col(T* W, int j, T (&x)[N]) {
+  __syncwarp(hw_mask());
+  if (j < N) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) W[i * LD + j] = x[i];
+  }
+  __syncwarp(hw_mask());
+  const int jr = j < N ? j : N - 1;
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = T(0.5) * (x[i] + W[jr * LD + i]);
+  __syncwarp(hw_mask());
+}
+
+// W <- G (row-major N x N global), cooperative over the half-warp.
+template <class T, int N, int LD>
+__device__ __forceinline__ void hw_load(T* W, const T* __restrict__ G, int l) {
+  __syncwarp(hw_mask());
+#pragma unroll
+  for (int idx = l; idx < N * N; idx += 16) W[(idx / N) * LD + idx % N] = G[idx];
+  __syncwarp(hw_mask());
+}
+
+// spd_inverse (schur.cpp:15-23): column j of sym((W)^{-1}); returns pivot / -1.
+template <class T, int N, int LD>
+__device__ __forceinline__ int hw_spd_inverse(T* W, T* rd, const T* __restrict__ G, int j,
+                                              T (&x)[N]) {
+  hw_load<T, N, LD>(W, G, j & 15);
+  const int f = hw_cholesky<T, N, LD>(W, rd, j);
+  hw_inv_col<T, N, LD>(W, rd, j < N ? j : 0, x);
+  hw_symmetrize_col<T, N, LD>(W, j, x);
+  return f;
+}
+
+template <class T>
+__device__ __forceinline__ T block_reduce(T v, T* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T s = T(0);
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// Formation-phase shared memory (elements): per-knot Q^-1, R^-1 and the
+// products Q^-1 q, R^-1 r, then per-half-warp scratch tiles.
+template <class T, int NB, int MB>
+struct FLayout {
+  static constexpr int LD = Odd<NB>::v;
+  static constexpr int LDM = Odd<MB>::v;
+  static constexpr int per_hw = NB * LD + NB * LDM + 32;  // tW, tBR, rd[16], v[16]
+  __host__ __device__ static int oQi(int) { return 0; }
+  __host__ __device__ static int oRi(int K) { return K * NB * NB; }
+  __host__ __device__ static int oqq(int K) { return oRi(K) + (K - 1) * MB * MB; }
+  __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
+  __host__ __device__ static int ohw(int K) { return orr(K) + (K - 1) * 8; }
+  __host__ __device__ static int total(int K) { return ohw(K) + kHalfWarps * per_hw; }
+};
+
+}  // namespace
+
+template <class T, int NB, int MB, int R>
+__global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using FL = FLayout<T, NB, MB>;
+  constexpr int NN = NB * NB;
+  constexpr int LD = FL::LD, LDM = FL::LDM;
+  const int K = p.K, N = K - 1;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int l = lane & 15;        // row inside the block
+  const int h = tid >> 4;         // half-warp index = owned block row (first)
+  const bool lact = l < NB;
+  T* smem = reinterpret_cast<T*>(smem_raw);
+  // PCG layout
+  T* sL = smem;                          // [K][NB][NB]
+  T* sD = sL + static_cast<size_t>(K) * NN;  // [K][NB][NB]
+  T* sp = sD + static_cast<size_t>(K) * NN;  // [K][NB]
+  T* st = sp + K * NB;
+  T* su = st + K * NB;
+  T* red = su + K * NB;                  // [64]
+  // formation layout (aliases the PCG layout; phases are separated by barriers)
+  T* sQi = smem + FL::oQi(K);   // [K][NB][NB], column l written by lane l
+  T* sRi = smem + FL::oRi(K);   // [N][MB][MB]
+  T* sqq = smem + FL::oqq(K);   // [K][16]  Q_k^-1 q_k
+  T* srr = smem + FL::orr(K);   // [N][8]   R_k^-1 r_k
+  __shared__ int s_err;
+  // CTA-private global slot (L2 resident)
+  T* gL = p.slot + static_cast<size_t>(blockIdx.x) * (3 * K * NN + K * NB);
+  T* gD = gL + static_cast<size_t>(K) * NN;
+  T* gT = gD + static_cast<size_t>(K) * NN;
+  T* gG = gT + static_cast<size_t>(K) * NN;  // gamma [K][NB]
+
+  for (int sys = blockIdx.x; sys < p.B; sys += gridDim.x) {
+    const size_t nn = NN, nm = NB * MB, mm = MB * MB;
+    const T* Qs = p.Q + static_cast<size_t>(sys) * K * nn;
+    const T* qs = p.q + static_cast<size_t>(sys) * K * NB;
+    const T* Rs = p.R + static_cast<size_t>(sys) * N * mm;
+    const T* rs = p.r + static_cast<size_t>(sys) * N * MB;
+    const T* As = p.A + static_cast<size_t>(sys) * N * nn;
+    const T* Bs = p.Bm + static_cast<size_t>(sys) * N * nm;
+    const T* es = p.e + static_cast<size_t>(sys) * N * NB;
+    const T* xs = p.x_s + static_cast<size_t>(sys) * NB;
+    const T* x0 = p.x0 + static_cast<size_t>(sys) * NB;
+
+    __syncthreads();  // previous system's PCG is done with shared memory
+    if (tid == 0) s_err = 0x7fffffff;
+
+    T* hw = smem + FL::ohw(K) + static_cast<size_t>(h) * FL::per_hw;
+    T* tW = hw;
+    T* tBR = tW + NB * LD;
+    T* rd = tBR + NB * LDM;
+    const int lr = lact ? l : NB - 1;
+    int fkey = 0x7fffffff;
+
+    // ============================================================ F1: knots
+    // Q_k^-1 for every knot and R_k^-1 for k < N, computed once and shared
+    // by the two block rows that use them (the reference recomputes them per
+    // row, schur.cpp:49-51; same arithmetic).
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const int k = h + r * kHalfWarps;
+      if (k < K) {
+        T x[NB];
+        const int f = hw_spd_inverse<T, NB, LD>(tW, rd, Qs + k * nn, l, x);
+        // first failing call in row order: row k (Q_{k+1} of row k, key 4k+2) or row 0
+        if (f >= 0) fkey = min(fkey, k == 0 ? 0 : 4 * k + 2);
+        if (lact) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) sQi[k * NN + i * NB + l] = x[i];
+          T qq = T(0);
+#pragma unroll
+          for (int i = 0; i < NB; ++i) qq += x[i] * qs[k * NB + i];
+          sqq[k * 16 + l] = qq;
+        }
+      }
+      if (k < N) {
+        T x[MB];
+        const int f = hw_spd_inverse<T, MB, LDM>(tW, rd, Rs + k * mm, l, x);
+        if (f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
+        if (l < MB) {
+#pragma unroll
+          for (int i = 0; i < MB; ++i) sRi[k * MB * MB + i * MB + l] = x[i];
+          T rr = T(0);
+#pragma unroll
+          for (int i = 0; i < MB; ++i) rr += x[i] * rs[k * MB + i];
+          srr[k * 8 + l] = rr;
+        }
+      }
+    }
+    __syncthreads();
+
+    // ============================================================ F2: rows
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const int b = h + r * kHalfWarps;
+      if (b >= K) continue;
+      if (b == 0) {
+        // schur.cpp:53-57: S(0,0) = Q0^-1, theta_inv[0] = sym(Q0), gamma_0
+        if (lact) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            gD[i * NB + l] = sQi[i * NB + l];
+            gT[l * NB + i] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
+          }
+          gG[l] = -((xs[l] - x0[l]) + sqq[l]);
+        }
+        continue;
+      }
+      const int k = b - 1;
+      const T* Ak = As + k * nn;
+      const T* Bk = Bs + k * nm;
+      T x[NB];
+      // AQ = A_k Q_k^-1, column l  ->  L_b = phi = -AQ   (schur.cpp:68)
+      {
+        T qc[NB];
+#pragma unroll
+        for (int q = 0; q < NB; ++q) qc[q] = sQi[k * NN + q * NB + lr];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          T s = T(0);
+#pragma unroll
+          for (int q = 0; q < NB; ++q) s += __ldg(Ak + i * NB + q) * qc[q];
+          x[i] = s;
+        }
+      }
+      __syncwarp(hw_mask());
+      if (lact) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          tW[i * LD + l] = x[i];
+          gL[static_cast<size_t>(b) * nn + i * NB + l] = -x[i];
+        }
+      }
+      // BR = B_k R_k^-1, column l < m
+      {
+        const int lm = l < MB ? l : MB - 1;
+        T rc[MB];
+#pragma unroll
+        for (int q = 0; q < MB; ++q) rc[q] = sRi[k * MB * MB + q * MB + lm];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          T s = T(0);
+#pragma unroll
+          for (int q = 0; q < MB; ++q) s += __ldg(Bk + i * MB + q) * rc[q];
+          if (l < MB) tBR[i * LDM + l] = s;
+        }
+      }
+      __syncwarp(hw_mask());
+      // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
+      T arow[NB], brow[MB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) arow[q] = __ldg(Ak + lr * NB + q);
+#pragma unroll
+      for (int q = 0; q < MB; ++q) brow[q] = __ldg(Bk + lr * MB + q);
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        T s1 = T(0), s2 = T(0);
+#pragma unroll
+        for (int q = 0; q < NB; ++q) s1 += tW[i * LD + q] * arow[q];
+#pragma unroll
+        for (int q = 0; q < MB; ++q) s2 += tBR[i * LDM + q] * brow[q];
+        x[i] = (s1 + s2) + sQi[(k + 1) * NN + i * NB + lr];
+      }
+      // zeta = -A (Q_k^-1 q_k) - B (R_k^-1 r_k) + Q_{k+1}^-1 q_{k+1}; gamma (schur.cpp:69-77)
+      {
+        T aqq = T(0), brr = T(0);
+#pragma unroll
+        for (int q = 0; q < NB; ++q) aqq += arow[q] * sqq[k * 16 + q];
+#pragma unroll
+        for (int q = 0; q < MB; ++q) brr += brow[q] * srr[k * 8 + q];
+        const T zeta = (-aqq - brr) + sqq[(k + 1) * 16 + lr];
+        if (lact) gG[static_cast<size_t>(b) * NB + l] = -(-__ldg(es + k * NB + l) + zeta);
+      }
+      hw_symmetrize_col<T, NB, LD>(tW, l, x);  // theta (schur.cpp:67)
+      if (lact) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          gD[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
+          tW[i * LD + l] = x[i];
+        }
+      }
+      __syncwarp(hw_mask());
+      // theta^-1 (schur.cpp:75)
+      {
+        const int f = hw_cholesky<T, NB, LD>(tW, rd, l);
+        if (f >= 0) fkey = min(fkey, b * 4 + 3);
+        hw_inv_col<T, NB, LD>(tW, rd, lact ? l : 0, x);
+        hw_symmetrize_col<T, NB, LD>(tW, l, x);
+      }
+      if (lact) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) gT[static_cast<size_t>(b) * nn + l * NB + i] = x[i];
+      }
+    }
+    if (l == 0 && fkey != 0x7fffffff) atomicMin(&s_err, fkey);
+    __syncthreads();
+    if (s_err != 0x7fffffff) {
+      if (tid == 0) {
+        p.errkey[sys] = s_err;
+        SysOut o{};
+        o.code = kRuntime;
+        o.which = kWhichNone;
+        o.iteration = -1;
+        p.out[sys] = o;
+      }
+      continue;
+    }
+    if (tid == 0 && p.errkey) p.errkey[sys] = 0x7f7f7f7f;
+
+    // ================================================================ P
+    // stage L, D into shared memory (16-byte vectors), theta^-1 rows -> registers
+    {
+      const int total2 = K * NN;  // doubles per matrix
+      const T* srcL = gL;
+      const T* srcD = gD;
+      for (int i = tid * 2; i < total2; i += kThreads * 2) {
+        *reinterpret_cast<double2*>(reinterpret_cast<double*>(sL) + i) =
+            __ldcg(reinterpret_cast<const double2*>(reinterpret_cast<const double*>(srcL) + i));
+        *reinterpret_cast<double2*>(reinterpret_cast<double*>(sD) + i) =
+            __ldcg(reinterpret_cast<const double2*>(reinterpret_cast<const double*>(srcD) + i));
+      }
+    }
+    T ti[R][NB];
+    T lam[R], rr[R], rt[R], pp[R], spv[R], best[R], gam[R];
+    int bb[R];
+    bool act[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      bb[r] = h + r * kHalfWarps;
+      act[r] = bb[r] < K && lact;
+      const int b = bb[r] < K ? bb[r] : K - 1;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) ti[r][i] = __ldcg(gT + static_cast<size_t>(b) * NN + (lact ? l : 0) * NB + i);
+      gam[r] = __ldcg(gG + b * NB + (lact ? l : 0));
+      lam[r] = (act[r] && p.lambda0) ? p.lambda0[static_cast<size_t>(sys) * K * NB + b * NB + l]
+                                     : T(0);
+      if (act[r]) sp[b * NB + l] = lam[r];
+    }
+    __syncthreads();
+
+    auto Srow = [&](int b, const T* x) -> T {
+      // ((D x_b + L x_{b-1}) + R x_{b+1}), R_b = L_{b+1}'  (block_tri.cpp:82-92)
+      const T* Dr = sD + static_cast<size_t>(b) * NN + l * NB;
+      const T* xb = x + b * NB;
+      T sd = T(0);
+#pragma unroll
+      for (int j = 0; j < NB; j += 2) {
+        const double2 m2 = *reinterpret_cast<const double2*>(Dr + j);
+        const double2 v2 = *reinterpret_cast<const double2*>(xb + j);
+        sd += m2.x * v2.x;
+        sd += m2.y * v2.y;
+      }
+      T out = sd;
+      if (b > 0) {
+        const T* Lr = sL + static_cast<size_t>(b) * NN + l * NB;
+        const T* xl = xb - NB;
+        T sl = T(0);
+#pragma unroll
+        for (int j = 0; j < NB; j += 2) {
+          const double2 m2 = *reinterpret_cast<const double2*>(Lr + j);
+          const double2 v2 = *reinterpret_cast<const double2*>(xl + j);
+          sl += m2.x * v2.x;
+          sl += m2.y * v2.y;
+        }
+        out += sl;
+      }
+      if (b + 1 < K) {
+        const T* Lc = sL + static_cast<size_t>(b + 1) * NN + l;
+        const T* xr = xb + NB;
+        T sr = T(0);
+#pragma unroll
+        for (int j = 0; j < NB; j += 2) {
+          const double2 v2 = *reinterpret_cast<const double2*>(xr + j);
+          sr += Lc[j * NB] * v2.x;
+          sr += Lc[(j + 1) * NB] * v2.y;
+        }
+        out += sr;
+      }
+      return out;
+    };
+    auto theta_apply = [&](const T (&tr)[NB], const T* v) -> T {
+      T s = T(0);
+#pragma unroll
+      for (int j = 0; j < NB; j += 2) {
+        const double2 v2 = *reinterpret_cast<const double2*>(v + j);
+        s += tr[j] * v2.x;
+        s += tr[j + 1] * v2.y;
+      }
+      return s;
+    };
+
+    // r = gamma - S lambda0 (pcg.cpp:62)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int b = bb[r] < K ? bb[r] : K - 1;
+      const T s = p.lambda0 ? Srow(b, sp) : T(0);
+      rr[r] = gam[r] - s;
+    }
+    // r~ = Phi^-1 r, for every kind
+    auto precondition = [&]() {
+      if (p.kind == kIdentity) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) rt[r] = rr[r];
+        return;
+      }
+      T tv[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r]) su[bb[r] * NB + l] = rr[r];
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int b = bb[r] < K ? bb[r] : K - 1;
+        tv[r] = theta_apply(ti[r], su + b * NB);
+      }
+      if (p.kind == kJacobi) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) rt[r] = tv[r];
+        return;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r]) st[bb[r] * NB + l] = tv[r];
+      __syncthreads();
+      T uv[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int b = bb[r] < K ? bb[r] : K - 1;
+        T v = rr[r];
+        if (b > 0) {
+          const T* Lr = sL + static_cast<size_t>(b) * NN + l * NB;
+          const T* tl = st + (b - 1) * NB;
+          T sl = T(0);
+#pragma unroll
+          for (int j = 0; j < NB; j += 2) {
+            const double2 m2 = *reinterpret_cast<const double2*>(Lr + j);
+            const double2 v2 = *reinterpret_cast<const double2*>(tl + j);
+            sl += m2.x * v2.x;
+            sl += m2.y * v2.y;
+          }
+          v -= sl;
+        }
+        if (b + 1 < K) {
+          const T* Lc = sL + static_cast<size_t>(b + 1) * NN + l;
+          const T* tr = st + (b + 1) * NB;
+          T sr = T(0);
+#pragma unroll
+          for (int j = 0; j < NB; j += 2) {
+            const double2 v2 = *reinterpret_cast<const double2*>(tr + j);
+            sr += Lc[j * NB] * v2.x;
+            sr += Lc[(j + 1) * NB] * v2.y;
+          }
+          v -= sr;
+        }
+        uv[r] = v;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r]) su[bb[r] * NB + l] = uv[r];
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int b = bb[r] < K ? bb[r] : K - 1;
+        const bool corr = (p.kind == kSymStair) || (b & 1);
+        rt[r] = corr ? theta_apply(ti[r], su + b * NB) : tv[r];
+      }
+    };
+    precondition();
+    T eta_part = T(0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      pp[r] = rt[r];
+      if (act[r]) eta_part += rr[r] * rt[r];
+      best[r] = lam[r];
+    }
+    T eta = block_reduce(eta_part, red);
+
+    int code = kOk, which = kWhichNone, err_iter = -1, iterations = 0, converged = 0;
+    double exit_eta = static_cast<double>(eta), value = 0.0;
+    T best_eta = eta;
+    double* trace = p.trace ? p.trace + static_cast<size_t>(sys) * p.trace_cap : nullptr;
+    if (!is_finite(eta)) {
+      code = kRuntime;
+      which = kWhichInitNonFinite;
+    } else if (static_cast<double>(eta) < p.epsilon) {
+      converged = 1;
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r]) sp[bb[r] * NB + l] = pp[r];
+      __syncthreads();
+      for (int it = 1; it <= p.max_iter; ++it) {
+        T up = T(0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int b = bb[r] < K ? bb[r] : K - 1;
+          spv[r] = Srow(b, sp);
+          if (act[r]) up += pp[r] * spv[r];
+        }
+        const T ups = block_reduce(up, red);
+        if (!is_finite(ups)) {
+          code = kRuntime;
+          which = kWhichUpsNonFinite;
+          err_iter = it;
+          break;
+        }
+        if (ups <= T(0)) {
+          code = kBreakdown;
+          which = kWhichBreakdown;
+          err_iter = it;
+          value = static_cast<double>(ups);
+          break;
+        }
+        const T alpha = eta / ups;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          rr[r] -= alpha * spv[r];
+          lam[r] += alpha * pp[r];
+        }
+        precondition();
+        T ep = T(0);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (act[r]) ep += rr[r] * rt[r];
+        const T eta_p = block_reduce(ep, red);
+        if (!is_finite(eta_p)) {
+          code = kRuntime;
+          which = kWhichEtaNonFinite;
+          err_iter = it;
+          break;
+        }
+        if (trace && tid == 0) trace[it - 1] = static_cast<double>(eta_p);
+        if (eta_p < best_eta) {
+          best_eta = eta_p;
+#pragma unroll
+          for (int r = 0; r < R; ++r) best[r] = lam[r];
+        }
+        iterations = it;
+        exit_eta = static_cast<double>(eta_p);
+        if (static_cast<double>(eta_p) < p.epsilon) {
+          converged = 1;
+          break;
+        }
+        if (it == p.max_iter) break;
+        const T beta = eta_p / eta;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          pp[r] = rt[r] + beta * pp[r];
+          if (act[r]) sp[bb[r] * NB + l] = pp[r];
+        }
+        eta = eta_p;
+        __syncthreads();
+      }
+    }
+    if (code == kOk) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (act[r])
+          p.lambda_out[static_cast<size_t>(sys) * K * NB + bb[r] * NB + l] =
+              converged ? lam[r] : best[r];
+    }
+    if (tid == 0) {
+      SysOut o;
+      o.code = code;
+      o.knot = -1;
+      o.which = which;
+      o.iteration = err_iter;
+      o.iterations = iterations;
+      o.converged = converged;
+      o.exit_eta = exit_eta;
+      o.value = value;
+      o.max_drift = 0.0;
+      o.trace_len = (trace && code == kOk) ? iterations : 0;
+      o._pad = 0;
+      p.out[sys] = o;
+    }
+  }
+}
+
+template <class T, int NB, int MB>
+size_t fused_smem_bytes(int K) {
+  using FL = FLayout<T, NB, MB>;
+  const size_t pcg = sizeof(T) * (static_cast<size_t>(2) * K * NB * NB + 3 * K * NB + 64);
+  const size_t form = sizeof(T) * static_cast<size_t>(FL::total(K));
+  return std::max(pcg, form);
+}
+
+template <class T>
+bool fused_supported(int K, int n, int m, int kind) {
+  if (!(n == 14 && m == 7)) return false;
+  if (sizeof(T) != 8) return false;
+  if (kind == kPoly) return false;
+  if (K < 2 || K > 2 * kHalfWarps) return false;
+  return fused_smem_bytes<T, 14, 7>(K) + 64 <= 227 * 1024;
+}
+
+template <class T>
+size_t fused_slot_elems(int K, int n) {
+  return static_cast<size_t>(3) * K * n * n + static_cast<size_t>(K) * n;
+}
+
+template <class T>
+cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st) {
+  if constexpr (sizeof(T) == 8) {
+    const size_t smem = fused_smem_bytes<T, 14, 7>(p.K);
+    if (p.K <= kHalfWarps) {
+      auto kern = k_fused_cta<T, 14, 7, 1>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kThreads, smem, st>>>(p);
+    } else {
+      auto kern = k_fused_cta<T, 14, 7, 2>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem));
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kThreads, smem, st>>>(p);
+    }
+    return cudaGetLastError();
+  } else {
+    return cudaErrorNotSupported;
+  }
+}
+
+template bool fused_supported<double>(int, int, int, int);
+template bool fused_supported<float>(int, int, int, int);
+template size_t fused_slot_elems<double>(int, int);
+template size_t fused_slot_elems<float>(int, int);
+template cudaError_t launch_fused<double>(const FusedParams<double>&, int, cudaStream_t);
+template cudaError_t launch_fused<float>(const FusedParams<float>&, int, cudaStream_t);
+
+}  // namespace b2p

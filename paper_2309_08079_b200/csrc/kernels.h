@@ -60,6 +60,25 @@ struct PcgParams {
   int check_drift;
 };
 
+// Fused persistent K1+K3 (one CTA per system; fused_kernels.cu).
+template <class T>
+struct FusedParams {
+  int B, K, kind;
+  const T *Q, *q, *R, *r, *A, *Bm, *e, *x_s, *x0;  // [B][...] b2p_kkt layout
+  T* slot;            // [gridDim.x][3][K][n][n] CTA-private L, D, theta^-1 staging
+  const T* lambda0;   // [B][D] or null
+  T* lambda_out;      // [B][D]
+  int* errkey;        // [B]
+  SysOut* out;        // [B]
+  double* trace;      // [B][trace_cap] or null
+  int trace_cap;
+  double epsilon;
+  int max_iter;
+};
+template <class T> bool fused_supported(int K, int n, int m, int kind);
+template <class T> size_t fused_slot_elems(int K, int n);
+template <class T> cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st);
+
 // Shared-memory footprint of one PCG CTA (bytes) for a parameter block.
 template <class T>
 size_t pcg_smem_bytes(const PcgParams<T>& p);
