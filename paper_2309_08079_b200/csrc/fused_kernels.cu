@@ -154,6 +154,65 @@ __device__ __forceinline__ T block_reduce(T v, T* red) {
   return s;
 }
 
+// ---------------------------------------------------------------- PCG row products
+// R independent block rows per thread are processed together (j outer, row
+// inner) with two partial sums per dot product: more independent DFMA chains
+// in flight per warp for the same shared-memory traffic.
+template <class T, int NB, int R>
+__device__ __forceinline__ void dots_row(const T* (&M)[R], const T* (&x)[R], T (&out)[R]) {
+  T a[R], c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) a[r] = c[r] = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double2 m2 = *reinterpret_cast<const double2*>(M[r] + j);
+      const double2 v2 = *reinterpret_cast<const double2*>(x[r] + j);
+      a[r] += m2.x * v2.x;
+      c[r] += m2.y * v2.y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = a[r] + c[r];
+}
+// out[r] = sum_j Mc[r][j*NB] * x[r][j]  (column of a row-major block: R_b = L_{b+1}')
+template <class T, int NB, int R>
+__device__ __forceinline__ void dots_col(const T* (&Mc)[R], const T* (&x)[R], T (&out)[R]) {
+  T a[R], c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) a[r] = c[r] = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double2 v2 = *reinterpret_cast<const double2*>(x[r] + j);
+      a[r] += Mc[r][j * NB] * v2.x;
+      c[r] += Mc[r][(j + 1) * NB] * v2.y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = a[r] + c[r];
+}
+// out[r] = ti[r] . v[r]  (theta^-1 row held in registers)
+template <class T, int NB, int R>
+__device__ __forceinline__ void dots_reg(const T (&ti)[R][NB], const T* (&v)[R], T (&out)[R]) {
+  T a[R], c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) a[r] = c[r] = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double2 v2 = *reinterpret_cast<const double2*>(v[r] + j);
+      a[r] += ti[r][j] * v2.x;
+      c[r] += ti[r][j + 1] * v2.y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = a[r] + c[r];
+}
+
 // Formation-phase shared memory (elements): per-knot Q^-1, R^-1 and the
 // products Q^-1 q, R^-1 r, then per-half-warp scratch tiles.
 template <class T, int NB, int MB>
@@ -292,7 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int i = 0; i < NB; ++i) {
           T s = T(0);
 #pragma unroll
-          for (int q = 0; q < NB; ++q) s += __ldg(Ak + i * NB + q) * qc[q];
+          for (int q = 0; q < NB; q += 2) {
+            const double2 a2 = __ldg(reinterpret_cast<const double2*>(Ak + i * NB + q));
+            s += a2.x * qc[q];
+            s += a2.y * qc[q + 1];
+          }
           x[i] = s;
         }
       }
@@ -322,7 +385,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
       T arow[NB], brow[MB];
 #pragma unroll
-      for (int q = 0; q < NB; ++q) arow[q] = __ldg(Ak + lr * NB + q);
+      for (int q = 0; q < NB; q += 2) {
+        const double2 a2 = __ldg(reinterpret_cast<const double2*>(Ak + lr * NB + q));
+        arow[q] = a2.x;
+        arow[q + 1] = a2.y;
+      }
 #pragma unroll
       for (int q = 0; q < MB; ++q) brow[q] = __ldg(Bk + lr * MB + q);
 #pragma unroll
@@ -411,63 +478,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     }
     __syncthreads();
 
-    auto Srow = [&](int b, const T* x) -> T {
-      // ((D x_b + L x_{b-1}) + R x_{b+1}), R_b = L_{b+1}'  (block_tri.cpp:82-92)
-      const T* Dr = sD + static_cast<size_t>(b) * NN + l * NB;
-      const T* xb = x + b * NB;
-      T sd = T(0);
+    int bc[R];  // clamped block row per owned row
 #pragma unroll
-      for (int j = 0; j < NB; j += 2) {
-        const double2 m2 = *reinterpret_cast<const double2*>(Dr + j);
-        const double2 v2 = *reinterpret_cast<const double2*>(xb + j);
-        sd += m2.x * v2.x;
-        sd += m2.y * v2.y;
-      }
-      T out = sd;
-      if (b > 0) {
-        const T* Lr = sL + static_cast<size_t>(b) * NN + l * NB;
-        const T* xl = xb - NB;
-        T sl = T(0);
+    for (int r = 0; r < R; ++r) bc[r] = bb[r] < K ? bb[r] : K - 1;
+    // y_r = ((D x_b + L x_{b-1}) + R x_{b+1}) for the R owned rows, R_b = L_{b+1}'
+    // (block_tri.cpp:82-92). Out-of-range neighbours are computed on
+    // in-bounds shared memory and discarded by the selects.
+    auto Srows = [&](const T* x, T (&y)[R]) {
+      const T *Mp[R], *Xp[R];
+      T sd[R], sl[R], sr[R];
 #pragma unroll
-        for (int j = 0; j < NB; j += 2) {
-          const double2 m2 = *reinterpret_cast<const double2*>(Lr + j);
-          const double2 v2 = *reinterpret_cast<const double2*>(xl + j);
-          sl += m2.x * v2.x;
-          sl += m2.y * v2.y;
-        }
-        out += sl;
+      for (int r = 0; r < R; ++r) {
+        Mp[r] = sD + static_cast<size_t>(bc[r]) * NN + l * NB;
+        Xp[r] = x + bc[r] * NB;
       }
-      if (b + 1 < K) {
-        const T* Lc = sL + static_cast<size_t>(b + 1) * NN + l;
-        const T* xr = xb + NB;
-        T sr = T(0);
+      dots_row<T, NB, R>(Mp, Xp, sd);
 #pragma unroll
-        for (int j = 0; j < NB; j += 2) {
-          const double2 v2 = *reinterpret_cast<const double2*>(xr + j);
-          sr += Lc[j * NB] * v2.x;
-          sr += Lc[(j + 1) * NB] * v2.y;
-        }
-        out += sr;
+      for (int r = 0; r < R; ++r) {
+        Mp[r] = sL + static_cast<size_t>(bc[r]) * NN + l * NB;
+        Xp[r] = x + (bc[r] - 1) * NB;
       }
-      return out;
-    };
-    auto theta_apply = [&](const T (&tr)[NB], const T* v) -> T {
-      T s = T(0);
+      dots_row<T, NB, R>(Mp, Xp, sl);
 #pragma unroll
-      for (int j = 0; j < NB; j += 2) {
-        const double2 v2 = *reinterpret_cast<const double2*>(v + j);
-        s += tr[j] * v2.x;
-        s += tr[j + 1] * v2.y;
+      for (int r = 0; r < R; ++r) {
+        Mp[r] = sL + static_cast<size_t>(bc[r] + 1) * NN + l;
+        Xp[r] = x + (bc[r] + 1) * NB;
       }
-      return s;
+      dots_col<T, NB, R>(Mp, Xp, sr);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        T out = sd[r];
+        if (bc[r] > 0) out += sl[r];
+        if (bc[r] + 1 < K) out += sr[r];
+        y[r] = out;
+      }
     };
 
     // r = gamma - S lambda0 (pcg.cpp:62)
+    {
+      T sl0[R];
+      if (p.lambda0) Srows(sp, sl0);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int b = bb[r] < K ? bb[r] : K - 1;
-      const T s = p.lambda0 ? Srow(b, sp) : T(0);
-      rr[r] = gam[r] - s;
+      for (int r = 0; r < R; ++r) rr[r] = gam[r] - (p.lambda0 ? sl0[r] : T(0));
     }
     // r~ = Phi^-1 r, for every kind
     auto precondition = [&]() {
@@ -477,15 +529,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         return;
       }
       T tv[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (act[r]) su[bb[r] * NB + l] = rr[r];
-      __syncwarp();
+      const T* Vp[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int b = bb[r] < K ? bb[r] : K - 1;
-        tv[r] = theta_apply(ti[r], su + b * NB);
+        if (act[r]) su[bb[r] * NB + l] = rr[r];
+        Vp[r] = su + bc[r] * NB;
       }
+      __syncwarp();
+      dots_reg<T, NB, R>(ti, Vp, tv);  // t = theta^-1 r
       if (p.kind == kJacobi) {
 #pragma unroll
         for (int r = 0; r < R; ++r) rt[r] = tv[r];
@@ -495,48 +546,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       for (int r = 0; r < R; ++r)
         if (act[r]) st[bb[r] * NB + l] = tv[r];
       __syncthreads();
-      T uv[R];
+      // u = r - L_b t_{b-1} - R_b t_{b+1}
+      T sl[R], sr[R];
+      {
+        const T *Mp[R], *Xp[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int b = bb[r] < K ? bb[r] : K - 1;
-        T v = rr[r];
-        if (b > 0) {
-          const T* Lr = sL + static_cast<size_t>(b) * NN + l * NB;
-          const T* tl = st + (b - 1) * NB;
-          T sl = T(0);
-#pragma unroll
-          for (int j = 0; j < NB; j += 2) {
-            const double2 m2 = *reinterpret_cast<const double2*>(Lr + j);
-            const double2 v2 = *reinterpret_cast<const double2*>(tl + j);
-            sl += m2.x * v2.x;
-            sl += m2.y * v2.y;
-          }
-          v -= sl;
+        for (int r = 0; r < R; ++r) {
+          Mp[r] = sL + static_cast<size_t>(bc[r]) * NN + l * NB;
+          Xp[r] = st + (bc[r] - 1) * NB;
         }
-        if (b + 1 < K) {
-          const T* Lc = sL + static_cast<size_t>(b + 1) * NN + l;
-          const T* tr = st + (b + 1) * NB;
-          T sr = T(0);
+        dots_row<T, NB, R>(Mp, Xp, sl);
 #pragma unroll
-          for (int j = 0; j < NB; j += 2) {
-            const double2 v2 = *reinterpret_cast<const double2*>(tr + j);
-            sr += Lc[j * NB] * v2.x;
-            sr += Lc[(j + 1) * NB] * v2.y;
-          }
-          v -= sr;
+        for (int r = 0; r < R; ++r) {
+          Mp[r] = sL + static_cast<size_t>(bc[r] + 1) * NN + l;
+          Xp[r] = st + (bc[r] + 1) * NB;
         }
-        uv[r] = v;
+        dots_col<T, NB, R>(Mp, Xp, sr);
       }
       __syncwarp();
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (act[r]) su[bb[r] * NB + l] = uv[r];
+      for (int r = 0; r < R; ++r) {
+        T v = rr[r];
+        if (bc[r] > 0) v -= sl[r];
+        if (bc[r] + 1 < K) v -= sr[r];
+        if (act[r]) su[bb[r] * NB + l] = v;
+      }
       __syncwarp();
+      T uv[R];
+      dots_reg<T, NB, R>(ti, Vp, uv);  // theta^-1 u
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int b = bb[r] < K ? bb[r] : K - 1;
-        const bool corr = (p.kind == kSymStair) || (b & 1);
-        rt[r] = corr ? theta_apply(ti[r], su + b * NB) : tv[r];
+        const bool corr = (p.kind == kSymStair) || (bc[r] & 1);
+        rt[r] = corr ? uv[r] : tv[r];
       }
     };
     precondition();
@@ -565,12 +606,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       __syncthreads();
       for (int it = 1; it <= p.max_iter; ++it) {
         T up = T(0);
+        Srows(sp, spv);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int b = bb[r] < K ? bb[r] : K - 1;
-          spv[r] = Srow(b, sp);
+        for (int r = 0; r < R; ++r)
           if (act[r]) up += pp[r] * spv[r];
-        }
         const T ups = block_reduce(up, red);
         if (!is_finite(ups)) {
           code = kRuntime;

@@ -9,9 +9,7 @@ tail -3 gpurun_out/bench.log
 if [ -n "${NCU:-}" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-latency > gpurun_out/ncu_launch_bench.log 2>&1; echo ncu1_rc=$?
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_pcg -s 1 -c 1 \
-    -o gpurun_out/prof_k3 python bench.py --steps 1 --warmup 1 --batch 1024 --no-e2e --no-cpu --no-latency > gpurun_out/ncu_full_k3.log 2>&1; echo ncu2_rc=$?
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_build_schur -s 1 -c 1 \
-    -o gpurun_out/prof_k1 python bench.py --steps 1 --warmup 1 --batch 1024 --no-e2e --no-cpu --no-latency > gpurun_out/ncu_full_k1.log 2>&1; echo ncu3_rc=$?
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 \
+    -o gpurun_out/prof_k13 python bench.py --steps 1 --warmup 1 --batch 296 --no-e2e --no-cpu --no-latency > gpurun_out/ncu_full_k3.log 2>&1; echo ncu2_rc=$?
 fi
 cat gpurun_out/smoke.log
