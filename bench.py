@@ -237,7 +237,9 @@ def run_b200(a, world, rank, local):
     N, n, m, B = a.knots - 1, a.nx, a.nu, a.batch
     D = (N + 1) * n
     cfg = PcgConfig(epsilon=a.eps)
-    seed0 = a.seed + rank * B
+    from paper_2309_08079_b200.sharding import max_over_ranks, weak_shard
+    first, _last = weak_shard(B, rank)
+    seed0 = a.seed + first  # system i of the job <- seed + i (bench-pcg rule)
 
     def pinned(shape, dt):
         return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
@@ -259,11 +261,7 @@ def run_b200(a, world, rank, local):
             dist.barrier()
 
     def allmax(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return max_over_ranks(x, dist, device=f"cuda:{local}")
 
     # warm-up (also validates every system once)
     reps = api.solve_batched_device(kd, lam_dev.data_ptr(), B, PrecondKind.symmetric_stair, 1,

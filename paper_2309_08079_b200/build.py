@@ -59,6 +59,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_adapter_test(force: bool = False) -> str:
+    """g++ the C++ adapter test (tests/cpp/test_adapter.cpp) against libb2p.so."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "tests", "cpp", "test_adapter.cpp")
+    hdr = os.path.join(root, "include", "trajopt_b200.hpp")
+    out = os.path.join(root, "build", "test_adapter")
+    if not force and not _stale(out, [src, hdr, LIB]):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(root, "include"),
+                           src, "-o", out, "-L", HERE, "-lb2p",
+                           "-Wl,-rpath,$ORIGIN/../paper_2309_08079_b200"])
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)
