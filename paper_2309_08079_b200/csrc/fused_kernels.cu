@@ -68,8 +68,8 @@ __device__ __forceinline__ int hw_cholesky(T* A, T* rd, int l) {
       if (fail < 0) fail = k;
       x = T(1);
     }
-    const T d = sqrt(x);
-    const T r = T(1) / d;
+    const T r = rsqrt(x);  // one MUFU sequence per pivot: 1/L(k,k) and L(k,k) = x * r
+    const T d = x * r;
     __syncwarp(hw_mask());
     if (l == k) {
       A[k * LD + k] = d;
@@ -140,6 +140,9 @@ __device__ __forceinline__ int hw_spd_inverse(T* W, T* rd, const T* __restrict__
   return f;
 }
 
+// Block sum with a single barrier: callers alternate between two `red`
+// buffers, and at least one other barrier separates two uses of the same
+// buffer, so no trailing barrier is needed before it is rewritten.
 template <class T>
 __device__ __forceinline__ T block_reduce(T v, T* red) {
 #pragma unroll
@@ -150,7 +153,6 @@ __device__ __forceinline__ T block_reduce(T v, T* red) {
   T s = T(0);
 #pragma unroll
   for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-  __syncthreads();
   return s;
 }
 
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
           if (act[r]) up += pp[r] * spv[r];
-        const T ups = block_reduce(up, red);
+        const T ups = block_reduce(up, red + 32);  // buffer B
         if (!is_finite(ups)) {
           code = kRuntime;
           which = kWhichUpsNonFinite;
