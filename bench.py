@@ -339,11 +339,11 @@ def run_b200(a, world, rank, local):
     hbm, peak_src = peaks()
     k1_avg = k1_ms / max(1, nsolves)
     k3_avg = k3_ms / max(1, nsolves)
-    fused = ctx.last_path() == 1
+    fused = ctx.last_path() >= 1  # 1: one-CTA fused kernel, 2: fused cluster kernel
     if fused:
         # one persistent launch does K1+K2+K3: its compulsory HBM bytes are the
         # KKT inputs in and lambda out (the L/D/theta^-1 staging stays in L2)
-        dom = "K13_fused"
+        dom = "K13_fused" if ctx.last_path() == 1 else "K13_fused_cluster"
         dom_ms = k1_avg + k3_avg
         dom_bytes = B * (alg["b_in"] + (N + 1) * n * 8)
     else:

@@ -354,6 +354,65 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   const int K = k->N + 1, n = k->n;
   const size_t nn = static_cast<size_t>(n) * n, D = static_cast<size_t>(K) * n;
   const bool drift = cfg && cfg->check_residual_drift && cfg->variant == B2P_SEQUENTIAL;
+  // Fused cluster kernel: default for single solves and for shapes the
+  // one-CTA fused kernel does not cover; B2P_FC=1 forces it, =0 disables it.
+  const int fc_env = env_int("B2P_FC", -1);
+  int fcG = drift ? 0 : fc_pick_g<T>(K, n, k->m, kind, B);
+  if (fcG > 0 && env_int("B2P_FC_G", 0) > 0) {
+    const int g = env_int("B2P_FC_G", 0);
+    if ((K + g - 1) / g <= 32 && (K + ((K + g - 1) / g) - 1) / ((K + g - 1) / g) == g) fcG = g;
+  }
+  const bool one_cta_ok = fused_supported<T>(K, n, k->m, kind);
+  const bool use_fc = fcG > 0 && env_int("B2P_FUSED", 1) &&
+                      (fc_env == 1 || (fc_env == -1 && (B == 1 || !one_cta_ok)));
+  if (use_fc) {
+    FusedParams<T> f{};
+    f.B = B;
+    f.K = K;
+    f.kind = kind;
+    f.Q = static_cast<const T*>(kv.Q);
+    f.q = static_cast<const T*>(kv.q);
+    f.R = static_cast<const T*>(kv.R);
+    f.r = static_cast<const T*>(kv.r);
+    f.A = static_cast<const T*>(kv.A);
+    f.Bm = static_cast<const T*>(kv.B);
+    f.e = static_cast<const T*>(kv.e);
+    f.x_s = static_cast<const T*>(kv.x_s);
+    f.x0 = static_cast<const T*>(kv.x0);
+    const int max_clusters = std::max(1, c->sm_count / fcG);
+    f.slot = static_cast<T*>(ws_get(c, "fc_slot", sizeof(T) * fcG * max_clusters *
+                                                       fc_slot_elems<T>(K, n, fcG)));
+    f.lambda0 = static_cast<const T*>(lambda0);
+    f.lambda_out = static_cast<T*>(lambda_out);
+    f.errkey = errkey;
+    f.out = outs_dev;
+    f.trace = trace_dev;
+    f.trace_cap = trace_cap;
+    f.epsilon = cfg ? cfg->epsilon : 1e-4;
+    const int mi = cfg ? cfg->max_iter : 0;
+    f.max_iter = mi > 0 ? mi : static_cast<int>(D);
+    if (time_it) {
+      if (!c->accounting) c->pool_used = 0;
+      if (c->pool_used + 3 > c->pool.size())
+        for (int q = 0; q < 3; ++q) {
+          cudaEvent_t e;
+          CK(cudaEventCreate(&e));
+          c->pool.push_back(e);
+        }
+      c->ev0 = c->pool[c->pool_used];
+      c->ev2 = c->pool[c->pool_used + 1];
+      c->ev1 = c->pool[c->pool_used + 2];
+      c->pool_used += 3;
+      CK(cudaEventRecord(c->ev0, st));
+      CK(cudaEventRecord(c->ev2, st));
+    }
+    CK(launch_fc<T>(f, fcG, max_clusters, st));
+    c->launches++;
+    c->last_path = 2;
+    c->phases = time_it;
+    if (time_it) CK(cudaEventRecord(c->ev1, st));
+    return;
+  }
   if (!drift && env_int("B2P_FUSED", 1) && fused_supported<T>(K, n, k->m, kind)) {
     // persistent one-CTA-per-system K1+K3 kernel (fused_kernels.cu)
     const int grid = std::max(1, std::min(B, c->sm_count));

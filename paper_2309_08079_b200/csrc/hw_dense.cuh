@@ -1,0 +1,198 @@
+// Half-warp (16-lane) dense helpers shared by the fused kernels
+// (fused_kernels.cu: one CTA per system; fc_kernels.cu: one cluster per
+// system). One 16-lane half-warp owns one n x n block (n <= 16): lane l owns
+// row / column l. Every shuffle and __syncwarp uses the half-warp's own lane
+// mask, so the two half-warps of a warp may take different branches.
+#pragma once
+
+#include "kernels.h"
+
+namespace b2p {
+namespace hwd {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int N>
+struct Odd {
+  static constexpr int v = N | 1;
+};
+
+// ---------------------------------------------------------------- half-warp dense helpers
+// Each 16-lane half-warp runs these independently (the two half-warps of a
+// warp may take different branches, e.g. block row 0 vs row 1), so every
+// shuffle / __syncwarp uses the half-warp's own lane mask. Lanes l >= N
+// compute on clamped data and never store.
+__device__ __forceinline__ unsigned hw_mask() {
+  return 0xffffu << (threadIdx.x & 16);
+}
+
+// In-place lower Cholesky of an N x N tile (stride LD, lower triangle read),
+// left-looking like Eigen's llt_inplace::unblocked. Returns the first failing
+// pivot (x <= 0; a NaN pivot passes, as in Eigen) or -1.
+template <class T, int N, int LD>
+__device__ __forceinline__ int hw_cholesky(T* A, T* rd, int l) {
+  // In-place lower Cholesky of an N x N tile (stride LD, lower triangle read),
+  // left-looking like Eigen's llt_inplace::unblocked; rd[k] = 1 / L(k,k).
+  // Returns the first failing pivot (x <= 0; a NaN pivot passes, as in Eigen)
+  // or -1. Divisions are replaced by one reciprocal per pivot.
+  int fail = -1;
+  const int lr = l < N ? l : N - 1;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    T s = A[lr * LD + k];
+#pragma unroll
+    for (int p = 0; p < k; ++p) s -= A[lr * LD + p] * A[k * LD + p];
+    T x = __shfl_sync(hw_mask(), s, k, 16);
+    if (x <= T(0)) {
+      if (fail < 0) fail = k;
+      x = T(1);
+    }
+    const T r = rsqrt(x);  // one MUFU sequence per pivot: 1/L(k,k) and L(k,k) = x * r
+    const T d = x * r;
+    __syncwarp(hw_mask());
+    if (l == k) {
+      A[k * LD + k] = d;
+      rd[k] = r;
+    } else if (l > k && l < N) {
+      A[l * LD + k] = s * r;
+    }
+    __syncwarp(hw_mask());
+  }
+  return fail;
+}
+
+// x = column j of (L L')^{-1} (forward then backward substitution against e_j).
+template <class T, int N, int LD>
+__device__ __forceinline__ void hw_inv_col(const T* L, const T* rd, int j, T (&x)[N]) {
+  // __syncwarp between rows stops the scheduler from hoisting all N^2/2
+  // tile loads ahead of the recurrence (register blow-up / spills).
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T s = (i == j) ? T(1) : T(0);
+#pragma unroll
+    for (int p = 0; p < i; ++p) s -= L[i * LD + p] * x[p];
+    x[i] = s * rd[i];
+    __syncwarp(hw_mask());
+  }
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    T s = x[i];
+#pragma unroll
+    for (int p = i + 1; p < N; ++p) s -= L[p * LD + i] * x[p];
+    x[i] = s * rd[i];
+    __syncwarp(hw_mask());
+  }
+}
+
+// column j of X -> column j of 0.5 (X + X') through the tile W (overwritten).
+template <class T, int N, int LD>
+__device__ __forceinline__ void hw_symmetrize_col(T* W, int j, T (&x)[N]) {
+  __syncwarp(hw_mask());
+  if (j < N) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) W[i * LD + j] = x[i];
+  }
+  __syncwarp(hw_mask());
+  const int jr = j < N ? j : N - 1;
+#pragma unroll
+  for (int i = 0; i < N; ++i) x[i] = T(0.5) * (x[i] + W[jr * LD + i]);
+  __syncwarp(hw_mask());
+}
+
+// W <- G (row-major N x N global), cooperative over the half-warp.
+template <class T, int N, int LD>
+__device__ __forceinline__ void hw_load(T* W, const T* __restrict__ G, int l) {
+  __syncwarp(hw_mask());
+#pragma unroll
+  for (int idx = l; idx < N * N; idx += 16) W[(idx / N) * LD + idx % N] = G[idx];
+  __syncwarp(hw_mask());
+}
+
+// spd_inverse (schur.cpp:15-23): column j of sym((W)^{-1}); returns pivot / -1.
+template <class T, int N, int LD>
+__device__ __forceinline__ int hw_spd_inverse(T* W, T* rd, const T* __restrict__ G, int j,
+                                              T (&x)[N]) {
+  hw_load<T, N, LD>(W, G, j & 15);
+  const int f = hw_cholesky<T, N, LD>(W, rd, j);
+  hw_inv_col<T, N, LD>(W, rd, j < N ? j : 0, x);
+  hw_symmetrize_col<T, N, LD>(W, j, x);
+  return f;
+}
+
+// Block sum with a single barrier: callers alternate between two `red`
+// buffers, and at least one other barrier separates two uses of the same
+// buffer, so no trailing barrier is needed before it is rewritten.
+template <class T, int kThreads = 512>
+__device__ __forceinline__ T block_reduce(T v, T* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  T s = T(0);
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+  return s;
+}
+
+// ---------------------------------------------------------------- PCG row products
+// R independent block rows per thread are processed together (j outer, row
+// inner) with two partial sums per dot product: more independent DFMA chains
+// in flight per warp for the same shared-memory traffic.
+template <class T, int NB, int R>
+__device__ __forceinline__ void dots_row(const T* (&M)[R], const T* (&x)[R], T (&out)[R]) {
+  T a[R], c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) a[r] = c[r] = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double2 m2 = *reinterpret_cast<const double2*>(M[r] + j);
+      const double2 v2 = *reinterpret_cast<const double2*>(x[r] + j);
+      a[r] += m2.x * v2.x;
+      c[r] += m2.y * v2.y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = a[r] + c[r];
+}
+// out[r] = sum_j Mc[r][j*NB] * x[r][j]  (column of a row-major block: R_b = L_{b+1}')
+template <class T, int NB, int R>
+__device__ __forceinline__ void dots_col(const T* (&Mc)[R], const T* (&x)[R], T (&out)[R]) {
+  T a[R], c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) a[r] = c[r] = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double2 v2 = *reinterpret_cast<const double2*>(x[r] + j);
+      a[r] += Mc[r][j * NB] * v2.x;
+      c[r] += Mc[r][(j + 1) * NB] * v2.y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = a[r] + c[r];
+}
+// out[r] = ti[r] . v[r]  (theta^-1 row held in registers)
+template <class T, int NB, int R>
+__device__ __forceinline__ void dots_reg(const T (&ti)[R][NB], const T* (&v)[R], T (&out)[R]) {
+  T a[R], c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) a[r] = c[r] = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double2 v2 = *reinterpret_cast<const double2*>(v[r] + j);
+      a[r] += ti[r][j] * v2.x;
+      c[r] += ti[r][j + 1] * v2.y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[r] = a[r] + c[r];
+}
+
+}  // namespace hwd
+}  // namespace b2p

@@ -79,6 +79,13 @@ template <class T> bool fused_supported(int K, int n, int m, int kind);
 template <class T> size_t fused_slot_elems(int K, int n);
 template <class T> cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st);
 
+// Fused cluster kernel (fc_kernels.cu): one thread-block cluster of G CTAs per
+// system. fc_pick_g returns the cluster size for a shape (0 = unsupported).
+template <class T> int fc_pick_g(int K, int n, int m, int kind, int B);
+template <class T> size_t fc_slot_elems(int K, int n, int G);
+template <class T>
+cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStream_t st);
+
 // Shared-memory footprint of one PCG CTA (bytes) for a parameter block.
 template <class T>
 size_t pcg_smem_bytes(const PcgParams<T>& p);

@@ -44,12 +44,12 @@ def timed(kkt, kind, eps, dtype=np.float64, env=None):
         t0 = time.perf_counter()
         orc_res = orc.solve(kkt, kind, 1, cfg, dtype=dtype)
         cpu_us = (time.perf_counter() - t0) * 1e6
-        path = api.context().last_path()
+        path = {0: "split K1+K3", 1: "fused one-CTA", 2: "fused cluster"}[api.context().last_path()]
         return {"us_median": statistics.median(ts), "us_min": min(ts),
                 "iterations": res.report.iterations,
                 "oracle_iterations": orc_res.report.iterations,
                 "iterations_equal": res.report.iterations == orc_res.report.iterations,
-                "cpu_oracle_1thread_us": cpu_us, "fused_kernel": bool(path == 1)}
+                "cpu_oracle_1thread_us": cpu_us, "path": path}
     finally:
         for k, v in saved.items():
             if v is None:
@@ -66,21 +66,34 @@ def main():
     out["c1_symstair_1e-8"] = timed(k1, PrecondKind.symmetric_stair, 1e-8)
     out["c1_symstair_1e-8_splitpath"] = timed(k1, PrecondKind.symmetric_stair, 1e-8,
                                               env={"B2P_FUSED": "0"})
+    out["c1_symstair_1e-8_onecta"] = timed(k1, PrecondKind.symmetric_stair, 1e-8,
+                                           env={"B2P_FC": "0"})
+    out["c1_symstair_1e-8_cluster2"] = timed(k1, PrecondKind.symmetric_stair, 1e-8,
+                                             env={"B2P_FC_G": "2"})
     k2 = orc.random_kkt(2, 127, 14, 7)
     for kind, name in [(PrecondKind.block_jacobi, "jacobi"), (PrecondKind.stair, "stair"),
                        (PrecondKind.symmetric_stair, "symstair")]:
         for eps in (1e-8, 1e-4):
             out[f"c2_{name}_{eps:g}"] = timed(k2, kind, eps)
+    out["c2_symstair_1e-8_cluster8"] = timed(k2, PrecondKind.symmetric_stair, 1e-8,
+                                             env={"B2P_FC_G": "8"})
+    out["c2_symstair_1e-8_split"] = timed(k2, PrecondKind.symmetric_stair, 1e-8,
+                                          env={"B2P_FC": "0"})
     k3 = orc.random_kkt(3, 255, 12, 4)
     for eps in (1e-4, 1e-6):
         out[f"c3_fp32_symstair_{eps:g}_auto"] = timed(k3, PrecondKind.symmetric_stair, eps,
                                                       dtype=np.float32)
+    for G in (8, 16):
+        out[f"c3_fp32_symstair_1e-4_fusedcluster{G}"] = timed(
+            k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32, env={"B2P_FC_G": str(G)})
     for G in (2, 4, 8):
-        out[f"c3_fp32_symstair_1e-4_cluster{G}"] = timed(
-            k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32, env={"B2P_PCG_G": str(G)})
+        out[f"c3_fp32_symstair_1e-4_split_cluster{G}"] = timed(
+            k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32,
+            env={"B2P_FC": "0", "B2P_PCG_G": str(G)})
     for G in (32, 64):
-        out[f"c3_fp32_symstair_1e-4_grid{G}"] = timed(
-            k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32, env={"B2P_PCG_G": str(G)})
+        out[f"c3_fp32_symstair_1e-4_split_grid{G}"] = timed(
+            k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32,
+            env={"B2P_FC": "0", "B2P_PCG_G": str(G)})
     k5 = orc.random_kkt(5, 511, 28, 14)
     out["c5_symstair_1e-8"] = timed(k5, PrecondKind.symmetric_stair, 1e-8)
     sweep = {}
