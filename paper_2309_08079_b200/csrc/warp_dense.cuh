@@ -57,10 +57,11 @@ __device__ int tcholesky(Tile<T> A, int n, int lane) {
     }
     const T x = __shfl_sync(kFull, s, k);
     if (x <= T(0)) return k;
-    const T d = sqrt(x);
+    const T r = rsqrt(x);  // 1/L(k,k); multiplications instead of divisions
+    const T d = x * r;
     __syncwarp();
     if (lane == k) A(k, k) = d;
-    else if (lane > k && lane < n) A(lane, k) = s / d;
+    else if (lane > k && lane < n) A(lane, k) = s * r;
     __syncwarp();
   }
   return -1;
@@ -72,15 +73,17 @@ template <class T>
 __device__ void tllt_inverse(Tile<T> L, Tile<T> X, int n, int lane) {
   if (lane < n) {
     const int j = lane;
-    for (int i = 0; i < n; ++i) {
+    // column j of L^-1 is zero above row j: start the forward sweep at j
+    for (int i = 0; i < j; ++i) X(i, j) = T(0);
+    for (int i = j; i < n; ++i) {
       T s = (i == j) ? T(1) : T(0);
-      for (int p = 0; p < i; ++p) s -= L(i, p) * X(p, j);
-      X(i, j) = s / L(i, i);
+      for (int p = j; p < i; ++p) s -= L(i, p) * X(p, j);
+      X(i, j) = s * (T(1) / L(i, i));
     }
     for (int i = n - 1; i >= 0; --i) {
       T s = X(i, j);
       for (int p = i + 1; p < n; ++p) s -= L(p, i) * X(p, j);
-      X(i, j) = s / L(i, i);
+      X(i, j) = s * (T(1) / L(i, i));
     }
   }
   __syncwarp();

@@ -44,12 +44,16 @@ def timed(kkt, kind, eps, dtype=np.float64, env=None):
         t0 = time.perf_counter()
         orc_res = orc.solve(kkt, kind, 1, cfg, dtype=dtype)
         cpu_us = (time.perf_counter() - t0) * 1e6
-        path = {0: "split K1+K3", 1: "fused one-CTA", 2: "fused cluster"}[api.context().last_path()]
+        ctx = api.context()
+        path = {0: "split K1+K3", 1: "fused one-CTA", 2: "fused cluster"}[ctx.last_path()]
+        k1_ms, k3_ms = ctx.last_phase_ms()
         return {"us_median": statistics.median(ts), "us_min": min(ts),
                 "iterations": res.report.iterations,
                 "oracle_iterations": orc_res.report.iterations,
                 "iterations_equal": res.report.iterations == orc_res.report.iterations,
-                "cpu_oracle_1thread_us": cpu_us, "path": path}
+                "cpu_oracle_1thread_us": cpu_us, "path": path,
+                "split_K1_us": k1_ms * 1e3 if path.startswith("split") else None,
+                "split_K3_us": k3_ms * 1e3 if path.startswith("split") else None}
     finally:
         for k, v in saved.items():
             if v is None:
