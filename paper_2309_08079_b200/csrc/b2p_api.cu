@@ -264,7 +264,9 @@ void run_pcg(b2p_ctx* c, PcgParams<T>& p, cudaStream_t st, bool time_it) {
   p.pub = static_cast<T*>(ws_get(c, "pcg_pub", sizeof(T) * D * p.B));
   p.slots = static_cast<T*>(ws_get(c, "pcg_slots", sizeof(T) * 2 * std::max(1, p.G) * p.B + 64));
   c->phases = false;
+  p.gbar = static_cast<unsigned*>(ws_get(c, "pcg_gbar", 256));
   if (time_it) CK(cudaEventRecord(c->ev0, st));
+  if (p.sync == kSyncGrid) CK(cudaMemsetAsync(p.gbar, 0, sizeof(unsigned), st));
   CK(launch_pcg<T>(p, st));
   c->launches++;
   if (time_it) CK(cudaEventRecord(c->ev1, st));
@@ -503,6 +505,8 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   p.best = static_cast<T*>(ws_get(c, tag + "best", sizeof(T) * Dall));
   p.pub = static_cast<T*>(ws_get(c, tag + "pub", sizeof(T) * Dall));
   p.slots = static_cast<T*>(ws_get(c, tag + "slots", sizeof(T) * 2 * p.G * B + 64));
+  p.gbar = static_cast<unsigned*>(ws_get(c, tag + "gbar", 256));
+  if (p.sync == kSyncGrid) CK(cudaMemsetAsync(p.gbar, 0, sizeof(unsigned), st));
   CK(launch_pcg<T>(p, st));
   c->launches++;
   if (time_it) CK(cudaEventRecord(c->ev1, st));

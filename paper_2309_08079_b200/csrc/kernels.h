@@ -58,6 +58,7 @@ struct PcgParams {
   double epsilon;
   int max_iter;
   int check_drift;
+  unsigned* gbar;  // kSyncGrid barrier counter (zeroed before the launch)
 };
 
 // Fused persistent K1+K3 (one CTA per system; fused_kernels.cu).

@@ -60,14 +60,32 @@ size_t pcg_smem_bytes(const PcgParams<T>& p) {
 
 namespace {
 
+// Grid barrier for the cooperative launch: one atomic arrive per CTA on a
+// monotonic counter (zeroed before the launch) and an acquire-load spin by
+// thread 0; bar.sync around it extends the ordering to the whole CTA.
+// (cooperative_groups' grid.sync measured ~30 us per barrier at 128 CTAs.)
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += gridDim.x;
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
 template <int SYNC>
-__device__ __forceinline__ void gsync() {
+__device__ __forceinline__ void gsync(unsigned* ctr, unsigned& target) {
   if constexpr (SYNC == kSyncCta) {
     __syncthreads();
   } else if constexpr (SYNC == kSyncCluster) {
     cg::this_cluster().sync();
   } else {
-    cg::this_grid().sync();
+    grid_barrier(ctr, target);
   }
 }
 
@@ -356,6 +374,7 @@ __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
   }
   if (p.errkey && p.errkey[sys] < 0x7f7f7f7f) return;  // formation failed (K1)
   Solver<T, MODE> s(p, sys, rank, smem_raw);
+  unsigned gtarget = 0;  // grid-barrier generation (kSyncGrid)
   const int K = p.K, nb = p.nb;
   const size_t D = static_cast<size_t>(K) * nb;
   const T* gam = p.gamma + sys * D;
@@ -368,10 +387,13 @@ __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
   const int ra = max(0, s.lo - hr), rc = min(K, s.hi + hr);  // rows carrying r / Sp
   const int own = (s.hi - s.lo) * nb;
 
+  // Sum of the G per-CTA partials: lane-parallel L2 loads and a fixed-order
+  // xor tree, computed redundantly by every warp of every CTA (bit-identical
+  // everywhere, no dependent chain of G global loads).
   auto reduce_slots = [&](T* slots) {
     T v = T(0);
-    for (int g = 0; g < p.G; ++g) v += __ldcg(slots + g);
-    return v;
+    for (int g = threadIdx.x & 31; g < p.G; g += 32) v += __ldcg(slots + g);
+    return warp_sum(v);
   };
 
   s.stage_in();
@@ -400,7 +422,7 @@ __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
   }
   if constexpr (SYNC != kSyncCta) {
     if (threadIdx.x == 0) slot_eta[rank] = eta;
-    gsync<SYNC>();
+    gsync<SYNC>(p.gbar, gtarget);
     eta = reduce_slots(slot_eta);
   }
 
@@ -424,7 +446,7 @@ __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
       T ups = s.dot_own(s.vp, s.vsp);
       if constexpr (SYNC != kSyncCta) {
         if (threadIdx.x == 0) slot_ups[rank] = ups;
-        gsync<SYNC>();
+        gsync<SYNC>(p.gbar, gtarget);
         ups = reduce_slots(slot_ups);
       }
       if (!is_finite(ups)) {
@@ -468,7 +490,7 @@ __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
       T eta_p = s.dot_own(s.vr, s.vrt);
       if constexpr (SYNC != kSyncCta) {
         if (threadIdx.x == 0) slot_eta[rank] = eta_p;
-        gsync<SYNC>();
+        gsync<SYNC>(p.gbar, gtarget);
         eta_p = reduce_slots(slot_eta);
       }
       if (!is_finite(eta_p)) {
