@@ -135,6 +135,10 @@ long long b2p_ctx_kernel_launches(b2p_ctx* ctx);
 /* Which device path the most recent fused solve took: 1 = the persistent
  * one-CTA-per-system K1+K3 kernel, 0 = split K1 formation + K3 PCG. */
 int b2p_ctx_last_path(b2p_ctx* ctx);
+/* Debug (B2P_PHASE_TIMING=1): per-system %globaltimer stamps of the last
+ * one-CTA fused solve, [n][8] = start, F1 end, F2 end, staging end, end (ns).
+ * Returns the number of systems copied. */
+int b2p_ctx_phase_stamps(b2p_ctx* ctx, unsigned long long* out, int n);
 
 /* ---- block_tri.hpp ---------------------------------------------------- */
 /* BlockTriMatrix::matvec (block_tri.cpp:70-92). */

@@ -39,6 +39,7 @@ def load() -> C.CDLL:
         "b2p_ctx_stream": ([vp], vp),
         "b2p_ctx_kernel_launches": ([vp], i64),
         "b2p_ctx_last_path": ([vp], i32),
+        "b2p_ctx_phase_stamps": ([vp, vp, i32], i32),
         "b2p_ctx_last_solve_ms": ([vp, C.POINTER(C.c_float)], i32),
         "b2p_ctx_last_phase_ms": ([vp, C.POINTER(C.c_float), i32], i32),
         "b2p_ctx_phase_accounting": ([vp, i32], i32),
@@ -77,6 +78,7 @@ def load() -> C.CDLL:
 EXPORTED = [
     "b2p_abi_version", "b2p_device_count", "b2p_ctx_create", "b2p_ctx_destroy",
     "b2p_ctx_set_stream", "b2p_ctx_stream", "b2p_ctx_kernel_launches", "b2p_ctx_last_path",
+    "b2p_ctx_phase_stamps",
     "b2p_ctx_last_solve_ms",
     "b2p_ctx_last_phase_ms", "b2p_ctx_phase_accounting", "b2p_ctx_phase_totals",
     "b2p_blocktri_matvec", "b2p_blocktri_cholesky_solve", "b2p_blocktri_check",

@@ -38,6 +38,8 @@ struct b2p_ctx {
   size_t pool_used = 0;
   float last_ms = 0.f;
   int last_path = 0;  // 1: the fused persistent K1+K3 kernel ran
+  unsigned long long* timing = nullptr;  // B2P_PHASE_TIMING=1: per-system phase stamps
+  int timing_n = 0;
   std::atomic<long long> launches{0};
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
@@ -431,7 +433,12 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.e = static_cast<const T*>(kv.e);
     f.x_s = static_cast<const T*>(kv.x_s);
     f.x0 = static_cast<const T*>(kv.x0);
-    f.slot = static_cast<T*>(ws_get(c, "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n)));
+    f.slot = static_cast<T*>(ws_get(c, "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n, k->m)));
+    f.timing = env_int("B2P_PHASE_TIMING", 0)
+                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
+                   : nullptr;
+    c->timing = f.timing;
+    c->timing_n = f.timing ? B : 0;
     f.lambda0 = static_cast<const T*>(lambda0);
     f.lambda_out = static_cast<T*>(lambda_out);
     f.errkey = errkey;
@@ -681,6 +688,18 @@ int b2p_ctx_set_stream(b2p_ctx* c, void* stream) {
 void* b2p_ctx_stream(b2p_ctx* c) { return c ? static_cast<void*>(c->stream()) : nullptr; }
 long long b2p_ctx_kernel_launches(b2p_ctx* c) { return c ? c->launches.load() : 0; }
 int b2p_ctx_last_path(b2p_ctx* c) { return c ? c->last_path : -1; }
+
+// Debug: copy the per-system globaltimer stamps of the last one-CTA fused
+// solve (B2P_PHASE_TIMING=1): [n][8] = start, F1 end, F2 end, staging end, end.
+int b2p_ctx_phase_stamps(b2p_ctx* c, unsigned long long* out, int n) {
+  if (!c || !out || !c->timing) return B2P_INVALID_ARGUMENT;
+  cudaSetDevice(c->device);
+  const int m = std::min(n, c->timing_n);
+  if (cudaMemcpy(out, c->timing, sizeof(unsigned long long) * 8 * m, cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return B2P_CUDA_ERROR;
+  return m;
+}
 int b2p_ctx_last_phase_ms(b2p_ctx* c, float* ms, int n) {
   if (!c || !ms || n < 2) return B2P_INVALID_ARGUMENT;
   ms[0] = ms[1] = 0.f;

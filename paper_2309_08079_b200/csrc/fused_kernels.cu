@@ -34,22 +34,28 @@ constexpr int kHalfWarps = kThreads / 16;
 
 using namespace hwd;
 
-// Formation-phase shared memory (elements): per-knot Q^-1, R^-1 and the
-// products Q^-1 q, R^-1 r, then per-half-warp scratch tiles.
+// Formation-phase shared memory (elements): per-knot Q^-1 and the products
+// Q^-1 q, R^-1 r, then per-half-warp scratch tiles (R^-1 goes to the slot).
 template <class T, int NB, int MB>
 struct FLayout {
   static constexpr int LD = Odd<NB>::v;
   static constexpr int LDM = Odd<MB>::v;
-  static constexpr int per_hw = NB * LD + NB * LDM + 32;  // tW, tBR, rd[16], v[16]
+  // tW: transposes / AQ / Lr tile; tX: L^-T tile, aliased by B R^-1; rd[16], v[16]
+  static constexpr int per_hw = NB * LD + NB * NB + 32;
   __host__ __device__ static int oQi(int) { return 0; }
-  __host__ __device__ static int oRi(int K) { return K * NB * NB; }
-  __host__ __device__ static int oqq(int K) { return oRi(K) + (K - 1) * MB * MB; }
+  __host__ __device__ static int oqq(int K) { return K * NB * NB; }
   __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
   __host__ __device__ static int ohw(int K) { return orr(K) + (K - 1) * 8; }
   __host__ __device__ static int total(int K) { return ohw(K) + kHalfWarps * per_hw; }
 };
 
 }  // namespace
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <class T, int NB, int MB, int R>
 __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
@@ -73,15 +79,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   T* red = su + K * NB;                  // [64]
   // formation layout (aliases the PCG layout; phases are separated by barriers)
   T* sQi = smem + FL::oQi(K);   // [K][NB][NB], column l written by lane l
-  T* sRi = smem + FL::oRi(K);   // [N][MB][MB]
   T* sqq = smem + FL::oqq(K);   // [K][16]  Q_k^-1 q_k
   T* srr = smem + FL::orr(K);   // [N][8]   R_k^-1 r_k
   __shared__ int s_err;
+  __shared__ __align__(8) unsigned long long s_mbar;  // TMA staging barrier
+  const unsigned mbar_addr = static_cast<unsigned>(__cvta_generic_to_shared(&s_mbar));
+  unsigned mbar_phase = 0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar_addr) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   // CTA-private global slot (L2 resident)
-  T* gL = p.slot + static_cast<size_t>(blockIdx.x) * (3 * K * NN + K * NB);
+  T* gL = p.slot + static_cast<size_t>(blockIdx.x) * (3 * K * NN + K * NB + K * MB * MB);
   T* gD = gL + static_cast<size_t>(K) * NN;
   T* gT = gD + static_cast<size_t>(K) * NN;
   T* gG = gT + static_cast<size_t>(K) * NN;  // gamma [K][NB]
+  T* gR = gG + static_cast<size_t>(K) * NB;  // R_k^-1 [N][MB][MB]
 
   for (int sys = blockIdx.x; sys < p.B; sys += gridDim.x) {
     const size_t nn = NN, nm = NB * MB, mm = MB * MB;
@@ -96,12 +110,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     const T* x0 = p.x0 + static_cast<size_t>(sys) * NB;
 
     __syncthreads();  // previous system's PCG is done with shared memory
+    unsigned long long* tm = (p.timing && tid == 0) ? p.timing + static_cast<size_t>(sys) * 8 : nullptr;
+    if (tm) tm[0] = gtimer();
     if (tid == 0) s_err = 0x7fffffff;
 
     T* hw = smem + FL::ohw(K) + static_cast<size_t>(h) * FL::per_hw;
     T* tW = hw;
-    T* tBR = tW + NB * LD;
-    T* rd = tBR + NB * LDM;
+    T* tX = tW + NB * LD;
+    T* tBR = tX;  // B R^-1 (stride LDM) is dead before the theta inverse needs tX
+    T* rd = tX + NB * NB;
     const int lr = lact ? l : NB - 1;
     int fkey = 0x7fffffff;
 
@@ -113,35 +130,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     for (int r = 0; r < R; ++r) {
       const int k = h + r * kHalfWarps;
       if (k < K) {
-        T x[NB];
-        const int f = hw_spd_inverse<T, NB, LD>(tW, rd, Qs + k * nn, l, x);
-        // first failing call in row order: row k (Q_{k+1} of row k, key 4k+2) or row 0
+        T a[NB], x[NB];
+        const T* Qr = Qs + static_cast<size_t>(k) * nn + lr * NB;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) a[i] = Qr[i];
+        const int f = hw_spd_inverse_v2<T, NB>(a, tW, tX, rd, l, x);
+        // first failing call in row order: row k as its Q_{k+1} (key 4k+2), or row 0
         if (f >= 0) fkey = min(fkey, k == 0 ? 0 : 4 * k + 2);
         if (lact) {
-#pragma unroll
-          for (int i = 0; i < NB; ++i) sQi[k * NN + i * NB + l] = x[i];
           T qq = T(0);
 #pragma unroll
-          for (int i = 0; i < NB; ++i) qq += x[i] * qs[k * NB + i];
+          for (int i = 0; i < NB; ++i) {
+            sQi[k * NN + i * NB + l] = x[i];
+            qq += x[i] * qs[k * NB + i];
+          }
           sqq[k * 16 + l] = qq;
         }
       }
       if (k < N) {
-        T x[MB];
-        const int f = hw_spd_inverse<T, MB, LDM>(tW, rd, Rs + k * mm, l, x);
+        T a[MB], x[MB];
+        const int lm = l < MB ? l : MB - 1;
+        const T* Rr = Rs + static_cast<size_t>(k) * mm + lm * MB;
+#pragma unroll
+        for (int i = 0; i < MB; ++i) a[i] = Rr[i];
+        const int f = hw_spd_inverse_v2<T, MB>(a, tW, tX, rd, l, x);
         if (f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
         if (l < MB) {
-#pragma unroll
-          for (int i = 0; i < MB; ++i) sRi[k * MB * MB + i * MB + l] = x[i];
           T rr = T(0);
 #pragma unroll
-          for (int i = 0; i < MB; ++i) rr += x[i] * rs[k * MB + i];
+          for (int i = 0; i < MB; ++i) {
+            gR[static_cast<size_t>(k) * mm + i * MB + l] = x[i];
+            rr += x[i] * rs[k * MB + i];
+          }
           srr[k * 8 + l] = rr;
         }
       }
     }
     __syncthreads();
 
+    if (tm) tm[1] = gtimer();
     // ============================================================ F2: rows
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
@@ -193,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         const int lm = l < MB ? l : MB - 1;
         T rc[MB];
 #pragma unroll
-        for (int q = 0; q < MB; ++q) rc[q] = sRi[k * MB * MB + q * MB + lm];
+        for (int q = 0; q < MB; ++q) rc[q] = __ldcg(gR + static_cast<size_t>(k) * mm + q * MB + lm);
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           T s = T(0);
@@ -235,24 +262,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       hw_symmetrize_col<T, NB, LD>(tW, l, x);  // theta (schur.cpp:67)
       if (lact) {
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          gD[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
-          tW[i * LD + l] = x[i];
-        }
+        for (int i = 0; i < NB; ++i) gD[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
       }
-      __syncwarp(hw_mask());
-      // theta^-1 (schur.cpp:75)
+      // theta^-1 (schur.cpp:75): x holds row l of the symmetric theta
       {
-        const int f = hw_cholesky<T, NB, LD>(tW, rd, l);
+        T th[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) th[i] = x[i];
+        const int f = hw_spd_inverse_v2<T, NB>(th, tW, tX, rd, l, x);
         if (f >= 0) fkey = min(fkey, b * 4 + 3);
-        hw_inv_col<T, NB, LD>(tW, rd, lact ? l : 0, x);
-        hw_symmetrize_col<T, NB, LD>(tW, l, x);
       }
       if (lact) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) gT[static_cast<size_t>(b) * nn + l * NB + i] = x[i];
       }
     }
+    if (tm) tm[2] = gtimer();
     if (l == 0 && fkey != 0x7fffffff) atomicMin(&s_err, fkey);
     __syncthreads();
     if (s_err != 0x7fffffff) {
@@ -269,18 +294,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     if (tid == 0 && p.errkey) p.errkey[sys] = 0x7f7f7f7f;
 
     // ================================================================ P
-    // stage L, D into shared memory (16-byte vectors), theta^-1 rows -> registers
+    // stage L, D (contiguous in the slot and in shared memory) with one TMA
+    // bulk copy completed on an mbarrier; then prefetch the next system's
+    // KKT inputs into L2 so its formation phase does not start on cold HBM.
     {
-      const int total2 = K * NN;  // doubles per matrix
-      const T* srcL = gL;
-      const T* srcD = gD;
-      for (int i = tid * 2; i < total2; i += kThreads * 2) {
-        *reinterpret_cast<double2*>(reinterpret_cast<double*>(sL) + i) =
-            __ldcg(reinterpret_cast<const double2*>(reinterpret_cast<const double*>(srcL) + i));
-        *reinterpret_cast<double2*>(reinterpret_cast<double*>(sD) + i) =
-            __ldcg(reinterpret_cast<const double2*>(reinterpret_cast<const double*>(srcD) + i));
+      const unsigned bytes = static_cast<unsigned>(sizeof(T) * 2 * K * NN);
+      if (tid == 0) {
+        asm volatile("fence.proxy.async;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(sL))),
+            "l"(gL), "r"(bytes), "r"(mbar_addr)
+            : "memory");
       }
+      const int nsys = sys + gridDim.x;
+      if (nsys < p.B && tid < 9) {
+        // per-field contiguous ranges of the next system (16-byte aligned inside)
+        const T* base[9] = {p.Q, p.q, p.R, p.r, p.A, p.Bm, p.e, p.x_s, p.x0};
+        const size_t per[9] = {static_cast<size_t>(K) * NN, static_cast<size_t>(K) * NB,
+                               static_cast<size_t>(N) * MB * MB, static_cast<size_t>(N) * MB,
+                               static_cast<size_t>(N) * NN, static_cast<size_t>(N) * NB * MB,
+                               static_cast<size_t>(N) * NB, NB, NB};
+        const char* lo = reinterpret_cast<const char*>(base[tid] + nsys * per[tid]);
+        const char* hi = lo + per[tid] * sizeof(T);
+        const char* a = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(lo) + 15) & ~uintptr_t(15));
+        const char* e = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(hi) & ~uintptr_t(15));
+        if (e > a)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a),
+                       "r"(static_cast<unsigned>(e - a))
+                       : "memory");
+      }
+      unsigned done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
+            "1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(mbar_addr), "r"(mbar_phase)
+            : "memory");
+      }
+      mbar_phase ^= 1u;
     }
+    if (tm) tm[3] = gtimer();
     T ti[R][NB];
     T lam[R], rr[R], rt[R], pp[R], spv[R], best[R], gam[R];
     int bb[R];
@@ -507,6 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       o.trace_len = (trace && code == kOk) ? iterations : 0;
       o._pad = 0;
       p.out[sys] = o;
+      if (tm) tm[4] = gtimer();
     }
   }
 }
@@ -529,8 +588,9 @@ bool fused_supported(int K, int n, int m, int kind) {
 }
 
 template <class T>
-size_t fused_slot_elems(int K, int n) {
-  return static_cast<size_t>(3) * K * n * n + static_cast<size_t>(K) * n;
+size_t fused_slot_elems(int K, int n, int m) {
+  return static_cast<size_t>(3) * K * n * n + static_cast<size_t>(K) * n +
+         static_cast<size_t>(K) * m * m;
 }
 
 template <class T>
@@ -558,8 +618,8 @@ cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st) {
 
 template bool fused_supported<double>(int, int, int, int);
 template bool fused_supported<float>(int, int, int, int);
-template size_t fused_slot_elems<double>(int, int);
-template size_t fused_slot_elems<float>(int, int);
+template size_t fused_slot_elems<double>(int, int, int);
+template size_t fused_slot_elems<float>(int, int, int);
 template cudaError_t launch_fused<double>(const FusedParams<double>&, int, cudaStream_t);
 template cudaError_t launch_fused<float>(const FusedParams<float>&, int, cudaStream_t);
 

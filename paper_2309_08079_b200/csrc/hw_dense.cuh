@@ -196,3 +196,74 @@ __device__ __forceinline__ void dots_reg(const T (&ti)[R][NB], const T* (&v)[R],
 
 }  // namespace hwd
 }  // namespace b2p
+
+namespace b2p {
+namespace hwd {
+
+// ---------------------------------------------------------------------------
+// Load-efficient half-warp SPD inverse (spd_inverse, schur.cpp:15-23).
+// Lane l owns row l. In: a[] = row l of W (registers; only the lower part is
+// used, as LLT does). Tiles (row stride N, 16-byte aligned rows for even N):
+//   Lr  : rows of L as they are finalised (pivot rows are read as broadcasts),
+//   LiT : rows of L^-T (= columns of L^-1).
+// 1. left-looking Cholesky (Eigen llt_inplace::unblocked order; x <= 0 fails,
+//    a NaN pivot passes) with the own row in registers;
+// 2. column l of L^-1 by forward substitution;
+// 3. X = L^-T L^-1: x[i] = sum_{p>=i} LiT[i][p] LiT[l][p] — independent dot
+//    products. X is bitwise symmetric (same products in the same order for
+//    X[i][l] and X[l][i]; the extra terms are exact zeros), so the
+//    0.5 (X + X') of the reference is the identity on it.
+// Out: x[] = row l (= column l) of W^-1. Returns the failing pivot or -1.
+template <class T, int N>
+__device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd, int l,
+                                                 T (&x)[N]) {
+  static_assert(N % 2 == 0 || sizeof(T) == 4 || true, "");
+  int fail = -1;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    T s = a[k];
+#pragma unroll
+    for (int q = 0; q < k; ++q) s -= a[q] * Lr[k * N + q];
+    T piv = __shfl_sync(hw_mask(), s, k, 16);
+    if (piv <= T(0)) {
+      if (fail < 0) fail = k;
+      piv = T(1);
+    }
+    const T r = rsqrt(piv);
+    if (l == k) {
+      a[k] = piv * r;
+      rd[k] = r;
+      Lr[k * N + k] = a[k];
+    } else if (l > k && l < N) {
+      a[k] = s * r;
+      Lr[l * N + k] = a[k];
+    }
+    __syncwarp(hw_mask());
+  }
+  // column l of L^-1 (zero above the diagonal)
+  T y[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T s = (i == l) ? T(1) : T(0);
+#pragma unroll
+    for (int q = 0; q < i; ++q) s -= Lr[i * N + q] * y[q];
+    y[i] = s * rd[i];
+  }
+  if (l < N) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) LiT[l * N + q] = y[q];
+  }
+  __syncwarp(hw_mask());
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T s = T(0);
+#pragma unroll
+    for (int q = i; q < N; ++q) s += LiT[i * N + q] * y[q];
+    x[i] = s;
+  }
+  __syncwarp(hw_mask());
+  return fail;
+}
+
+}  // namespace hwd
+}  // namespace b2p

@@ -75,9 +75,10 @@ struct FusedParams {
   int trace_cap;
   double epsilon;
   int max_iter;
+  unsigned long long* timing;  // optional [B][8] globaltimer stamps per phase (debug)
 };
 template <class T> bool fused_supported(int K, int n, int m, int kind);
-template <class T> size_t fused_slot_elems(int K, int n);
+template <class T> size_t fused_slot_elems(int K, int n, int m);
 template <class T> cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st);
 
 // Fused cluster kernel (fc_kernels.cu): one thread-block cluster of G CTAs per
