@@ -30,6 +30,7 @@ struct b2p_ctx {
   cudaStream_t user = nullptr;
   cudaStream_t aux = nullptr;  // second pipeline stream for batched host calls
   std::map<std::string, std::pair<void*, size_t>> ws;
+  std::map<std::string, std::pair<void*, size_t>> hws;  // pinned host staging
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;  // start, end, formation end
   bool phases = false;
   // phase accounting: one (start, formation end, end) event triple per fused solve
@@ -129,6 +130,30 @@ void* ws_get(b2p_ctx* c, const std::string& name, size_t bytes) {
     slot.second = bytes;
   }
   return slot.first;
+}
+
+// Pinned host staging buffer: a D2H into pageable memory blocks the host
+// thread until the copy (and every kernel before it) is done, which would
+// serialise the chunked H2D/compute pipeline of b2p_solve_batched.
+void* hws_get(b2p_ctx* c, const std::string& name, size_t bytes) {
+  auto& slot = c->hws[name];
+  if (slot.second < bytes) {
+    if (slot.first) CK(cudaFreeHost(slot.first));
+    slot.first = nullptr;
+    slot.second = 0;
+    if (bytes) CK(cudaMallocHost(&slot.first, bytes));
+    slot.second = bytes;
+  }
+  return slot.first;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
 }
 
 void h2d(b2p_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st) {
@@ -674,6 +699,8 @@ void b2p_ctx_destroy(b2p_ctx* c) {
   cudaStreamSynchronize(c->aux);
   for (auto& kv : c->ws)
     if (kv.second.first) cudaFree(kv.second.first);
+  for (auto& kv : c->hws)
+    if (kv.second.first) cudaFreeHost(kv.second.first);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   cudaStreamDestroy(c->own);
   cudaStreamDestroy(c->aux);
@@ -1164,11 +1191,16 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
     const size_t es = esize(dtype);
     const int K = k->N + 1, n = k->n;
     const size_t D = size_t(K) * n;
-    const int chunk = std::min(batch, std::max(1, env_int("B2P_BATCH_CHUNK", 1024)));
+    const int chunk = std::min(batch, std::max(1, env_int("B2P_BATCH_CHUNK", 512)));
     const int nchunks = (batch + chunk - 1) / chunk;
     cudaStream_t streams[2] = {c->stream(), c->aux};
-    std::vector<SysOut> outs(batch);
-    std::vector<int> keys(batch);
+    // per-system status words land in pinned staging (asynchronous D2H); so
+    // does lambda when the caller's buffer is pageable
+    SysOut* h_outs = static_cast<SysOut*>(hws_get(c, "bh_outs", sizeof(SysOut) * batch));
+    int* h_keys = static_cast<int*>(hws_get(c, "bh_keys", sizeof(int) * batch));
+    const bool lam_pinned = is_pinned(lambda_out);
+    char* h_lam = lam_pinned ? static_cast<char*>(lambda_out)
+                             : static_cast<char*>(hws_get(c, "bh_lam", es * D * batch));
     cudaEvent_t start = nullptr, stop = nullptr;
     CK(cudaEventCreate(&start));
     CK(cudaEventCreate(&stop));
@@ -1196,9 +1228,9 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
       else
         solve_device_impl<float>(c, &kc, kv, cnt, kind, order, cfg, dl0, dl, dout, ek, nullptr, 0,
                                  st, false, tag);
-      d2h(c, static_cast<char*>(lambda_out) + es * D * first, dl, es * D * cnt, st);
-      d2h(c, outs.data() + first, dout, sizeof(SysOut) * cnt, st);
-      d2h(c, keys.data() + first, ek, sizeof(int) * cnt, st);
+      d2h(c, h_lam + es * D * first, dl, es * D * cnt, st);
+      d2h(c, h_outs + first, dout, sizeof(SysOut) * cnt, st);
+      d2h(c, h_keys + first, ek, sizeof(int) * cnt, st);
     }
     cudaEvent_t join = nullptr;
     CK(cudaEventCreate(&join));
@@ -1210,6 +1242,9 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
     cudaEventDestroy(start);
     cudaEventDestroy(stop);
     cudaEventDestroy(join);
+    if (!lam_pinned) std::memcpy(lambda_out, h_lam, es * D * batch);
+    std::vector<SysOut> outs(h_outs, h_outs + batch);
+    std::vector<int> keys(h_keys, h_keys + batch);
     Fail firstf{B2P_OK, ""};
     resolve(outs, keys, batch, reports, c->last_ms * 1e-3 / batch, &firstf);
     if (firstf.code != B2P_OK) throw firstf;

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
             gD[i * NB + l] = sQi[i * NB + l];
-            gT[l * NB + i] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
+            gT[i * NB + l] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
           }
           gG[l] = -((xs[l] - x0[l]) + sqq[l]);
         }
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       }
       if (lact) {
 #pragma unroll
-        for (int i = 0; i < NB; ++i) gT[static_cast<size_t>(b) * nn + l * NB + i] = x[i];
+        for (int i = 0; i < NB; ++i) gT[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
       }
     }
     if (tm) tm[2] = gtimer();
@@ -327,16 +327,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
                        "r"(static_cast<unsigned>(e - a))
                        : "memory");
       }
-      unsigned done = 0;
-      while (!done) {
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
-            "1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(mbar_addr), "r"(mbar_phase)
-            : "memory");
-      }
-      mbar_phase ^= 1u;
     }
     if (tm) tm[3] = gtimer();
     T ti[R][NB];
@@ -348,12 +338,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       bb[r] = h + r * kHalfWarps;
       act[r] = bb[r] < K && lact;
       const int b = bb[r] < K ? bb[r] : K - 1;
+      // theta^-1 row l, stored transposed by F2 (coalesced both ways)
 #pragma unroll
-      for (int i = 0; i < NB; ++i) ti[r][i] = __ldcg(gT + static_cast<size_t>(b) * NN + (lact ? l : 0) * NB + i);
+      for (int i = 0; i < NB; ++i) ti[r][i] = __ldcg(gT + static_cast<size_t>(b) * NN + i * NB + (lact ? l : 0));
       gam[r] = __ldcg(gG + b * NB + (lact ? l : 0));
       lam[r] = (act[r] && p.lambda0) ? p.lambda0[static_cast<size_t>(sys) * K * NB + b * NB + l]
                                      : T(0);
       if (act[r]) sp[b * NB + l] = lam[r];
+    }
+    {
+      unsigned done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
+            "1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(mbar_addr), "r"(mbar_phase)
+            : "memory");
+      }
+      mbar_phase ^= 1u;
     }
     __syncthreads();
 
