@@ -316,22 +316,28 @@ def run_b200(a, world, rank, local):
                "path": "b2p_solve_batched (host pinned buffers, 2-stream chunked H2D/compute/D2H)"}
         ctx_h.close()
 
-    # ---- single-solve latency (c1: K=32 knots, n14 m7, fp64, eps 1e-8)
+    # ---- single-solve latency at the BASELINE single-system configs:
+    # device time (CUDA events around the solve kernel), median of 20 after 5 warm-up
     latency = None
     if not a.no_latency and rank == 0:
-        k1 = api.random_kkt(1, 31, 14, 7)
-        c1cfg = PcgConfig(epsilon=1e-8)
-        lat = []
-        it1 = 0
-        for i in range(25):
-            r = api.solve(k1, PrecondKind.symmetric_stair, 1, c1cfg)
-            if i >= 5:
-                lat.append(r.report.wall_time * 1e6)
-            it1 = r.report.iterations
-        latency = {"c1_us_median": statistics.median(lat), "c1_us_min": min(lat),
-                   "c1_iterations": it1,
-                   "what": "device time (CUDA events) of K1+K3 for one K=32 n=14 m=7 system; "
-                           "host copies excluded"}
+        latency = {"what": "device time (CUDA events) of one fused formation + PCG solve; "
+                           "host copies excluded; median of 20 after 5 warm-up solves"}
+        cases = {"c1": (1, 31, 14, 7, np.float64, 1e-8), "c2": (2, 127, 14, 7, np.float64, 1e-8),
+                 "c3": (3, 255, 12, 4, np.float32, 1e-4), "c5": (5, 511, 28, 14, np.float64, 1e-8)}
+        names = {0: "split", 1: "one-CTA fused", 2: "fused cluster", 3: "fused grid"}
+        for name, (seed, Nk, nk, mk, dt, eps) in cases.items():
+            kk = api.random_kkt(seed, Nk, nk, mk)
+            lat = []
+            r = None
+            for i in range(25):
+                r = api.solve(kk, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=eps), dtype=dt)
+                if i >= 5:
+                    lat.append(r.report.wall_time * 1e6)
+            latency[name] = {"us_median": statistics.median(lat), "us_min": min(lat),
+                             "iterations": r.report.iterations, "knots": Nk + 1, "nx": nk, "nu": mk,
+                             "dtype": np.dtype(dt).name, "epsilon": eps,
+                             "kernel": names.get(api.context().last_path(), "?")}
+        latency["c1_us_median"] = latency["c1"]["us_median"]
 
     # ---- roofline for the dominant kernel
     mean_iters = float(np.mean(iters))

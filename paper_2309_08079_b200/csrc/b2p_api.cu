@@ -38,7 +38,8 @@ struct b2p_ctx {
   std::vector<cudaEvent_t> pool;
   size_t pool_used = 0;
   float last_ms = 0.f;
-  int last_path = 0;  // 1: the fused persistent K1+K3 kernel ran
+  unsigned fg_epoch = 0;  // next LL epoch of the fused grid kernel
+  int last_path = 0;  // 0: split K1(+K2)+K3, 1: one-CTA fused, 2: fused cluster, 3: fused grid
   unsigned long long* timing = nullptr;  // B2P_PHASE_TIMING=1: per-system phase stamps
   int timing_n = 0;
   std::atomic<long long> launches{0};
@@ -392,8 +393,95 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     if ((K + g - 1) / g <= 32 && (K + ((K + g - 1) / g) - 1) / ((K + g - 1) / g) == g) fcG = g;
   }
   const bool one_cta_ok = fused_supported<T>(K, n, k->m, kind);
+  // Fused grid kernel: one long-horizon system over G co-resident CTAs (the
+  // default for shapes no cluster / one-CTA kernel covers, e.g. c5);
+  // B2P_FG=1 forces it, =0 disables it; B2P_FG_RP picks the rows per CTA.
+  const int fg_env = env_int("B2P_FG", -1);
+  const int fgRp = (drift || B > 8) ? 0
+                                    : fg_pick_rp<T>(K, n, k->m, kind, c->sm_count,
+                                                    env_int("B2P_FG_RP", 0));
+  // Single-solve policy (scripts/latency_sweep.py, profiles/r01_latency_sweep.json):
+  // short horizons (K <= 32) on one CTA, long fp64 horizons on the grid kernel,
+  // fp32 / other shapes on the cluster kernel.
+  const bool single_short = B == 1 && K <= 32 && one_cta_ok;
+  const bool use_fg = fgRp > 0 && env_int("B2P_FUSED", 1) &&
+                      (fg_env == 1 ||
+                       (fg_env == -1 && ((fcG == 0 && !one_cta_ok) ||
+                                         (B == 1 && !single_short && sizeof(T) == 8 &&
+                                          fc_env != 1))));
+  if (use_fg) {
+    FusedParams<T> f{};
+    f.B = B;
+    f.K = K;
+    f.kind = kind;
+    f.Q = static_cast<const T*>(kv.Q);
+    f.q = static_cast<const T*>(kv.q);
+    f.R = static_cast<const T*>(kv.R);
+    f.r = static_cast<const T*>(kv.r);
+    f.A = static_cast<const T*>(kv.A);
+    f.Bm = static_cast<const T*>(kv.B);
+    f.e = static_cast<const T*>(kv.e);
+    f.x_s = static_cast<const T*>(kv.x_s);
+    f.x0 = static_cast<const T*>(kv.x0);
+    f.lambda0 = static_cast<const T*>(lambda0);
+    f.lambda_out = static_cast<T*>(lambda_out);
+    f.errkey = errkey;
+    f.out = outs_dev;
+    f.trace = trace_dev;
+    f.trace_cap = trace_cap;
+    f.epsilon = cfg ? cfg->epsilon : 1e-4;
+    const int mi = cfg ? cfg->max_iter : 0;
+    f.max_iter = mi > 0 ? mi : static_cast<int>(D);
+    const int G = (K + fgRp - 1) / fgRp;
+    FgSync<T> sy{};
+    sy.gstride = (G + 31) / 32 * 32;
+    sy.n = n;
+    // LL slots: 16 bytes per value. Zeroed when (re)allocated; afterwards each
+    // launch starts at a fresh epoch so words of earlier launches never match.
+    const size_t slots = static_cast<size_t>(sy.gstride) * (2 * 8 + 2 * 2 * 32);
+    const size_t bytes = slots * 16;
+    void* cur = c->ws.count(tag + "fg_ll") ? c->ws[tag + "fg_ll"].first : nullptr;
+    unsigned long long* ll = static_cast<unsigned long long*>(ws_get(c, tag + "fg_ll", bytes));
+    const unsigned need = static_cast<unsigned>(
+        std::min<long long>(1ll << 30, 3ll * (f.max_iter + 4) * B + 16));
+    if (ll != cur || c->fg_epoch == 0 || c->fg_epoch > (1u << 31) - need) {
+      CK(cudaMemsetAsync(ll, 0, c->ws[tag + "fg_ll"].second, st));
+      c->fg_epoch = 1;
+    }
+    sy.epoch0 = c->fg_epoch;
+    c->fg_epoch += need;
+    sy.red = ll;
+    sy.xt = ll + 2 * 16 * static_cast<size_t>(sy.gstride);
+    sy.xr = sy.xt + 2 * static_cast<size_t>(sy.gstride) * 2 * 32;
+    if (time_it) {
+      if (!c->accounting) c->pool_used = 0;
+      if (c->pool_used + 3 > c->pool.size())
+        for (int q = 0; q < 3; ++q) {
+          cudaEvent_t e;
+          CK(cudaEventCreate(&e));
+          c->pool.push_back(e);
+        }
+      c->ev0 = c->pool[c->pool_used];
+      c->ev2 = c->pool[c->pool_used + 1];
+      c->ev1 = c->pool[c->pool_used + 2];
+      c->pool_used += 3;
+      CK(cudaEventRecord(c->ev0, st));
+      CK(cudaEventRecord(c->ev2, st));
+    }
+    f.timing = env_int("B2P_PHASE_TIMING", 0)
+                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
+                   : nullptr;
+    c->timing = f.timing;
+    c->timing_n = f.timing ? B : 0;
+    CK(launch_fg<T>(f, sy, fgRp, st));
+    c->launches++;
+    c->last_path = 3;
+    c->phases = time_it;
+    if (time_it) CK(cudaEventRecord(c->ev1, st));
+    return;
+  }
   const bool use_fc = fcG > 0 && env_int("B2P_FUSED", 1) &&
-                      (fc_env == 1 || (fc_env == -1 && (B == 1 || !one_cta_ok)));
+                      (fc_env == 1 || (fc_env == -1 && ((B == 1 && !single_short) || !one_cta_ok)));
   if (use_fc) {
     FusedParams<T> f{};
     f.B = B;

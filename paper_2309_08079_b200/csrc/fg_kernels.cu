@@ -1,0 +1,752 @@
+// Fused grid kernel (FG) — formation + stair-family PCG for ONE long-horizon
+// system spread over G co-resident CTAs (cooperative launch), e.g. c5:
+// K = 512 knots, n = 28, m = 14, fp64 on 128 CTAs of 4 block rows each.
+// Replaces build_schur (proj/src/schur.cpp:38-82), the stair-family builders
+// (:98-142) and pcg_solve (proj/src/pcg.cpp:55-129) in one launch.
+//
+// Layout: CTA c owns block rows [lo, hi) = [c*rp, min(K, (c+1)*rp)); warp w
+// owns block row b = lo + w and lane l < n owns scalar row l. One extra warp
+// per CTA (w = rp) recomputes the two knots the CTA shares with its
+// neighbours — Q_{lo-1}^-1, R_{lo-1}^-1 (row lo needs them) and
+// L_hi = -A_{hi-1} Q_{hi-1}^-1 (the column product R_{hi-1} = L_hi') — with
+// the same arithmetic on the same inputs as the owning CTA, so formation needs
+// no inter-CTA communication at all and S stays bitwise structurally
+// symmetric across CTA boundaries.
+//
+// Per PCG iteration three synchronisation points (the reference has six
+// barriers):
+//   * upsilon = p'Sp   — grid reduce-barrier (each CTA publishes its partial
+//     with an epoch; every CTA reads all G partials and sums them in one
+//     fixed order, so all CTAs hold bit-identical scalars, no atomics);
+//   * t = theta^-1 r   — neighbour-only flag exchange of the two boundary rows;
+//   * eta' = r'r~      — grid reduce-barrier; the boundary rows of r~ are
+//     published with it so p's halo rows are recomputed locally
+//     (p_halo = r~_halo + beta p_halo, the owner's arithmetic on the owner's
+//     data, bitwise equal).
+// Registers per lane: row l of L_b and of theta_b^-1; D_b and the L blocks
+// for the column products live in shared memory.
+#include <climits>
+
+#include "kernels.h"
+#include "wp_dense.cuh"
+
+namespace b2p {
+namespace {
+
+using namespace wpd;
+
+template <class T, int NB, int MB>
+struct FgLayout {
+  static constexpr int A = 16 / static_cast<int>(sizeof(T));  // elements per 16 bytes
+  static constexpr int pad(int x) { return (x + A - 1) / A * A; }
+  static constexpr int NN = NB * NB, MM = MB * MB, NM = NB * MB;
+  static constexpr int VS = pad(NB);
+  static constexpr int pNN = pad(NN), pMM = pad(MM), pNM = pad(NM);
+  // per-warp formation tile
+  static constexpr int oQt = 0, oRt = pNN, oAt = oRt + pMM, oBt = oAt + pNN, oLr = oBt + pNM,
+                       oLi = oLr + pNN, ord = oLi + pNN, oqq = ord + 32, orr = oqq + 32,
+                       FT = orr + 32;
+  __host__ __device__ static int tile(int w) { return w * FT; }
+  // PCG region (after the rp + 1 formation tiles)
+  __host__ __device__ static int oD(int rp) { return (rp + 1) * FT; }
+  __host__ __device__ static int oL(int rp) { return oD(rp) + rp * pNN; }
+  __host__ __device__ static int oP(int rp) { return oL(rp) + (rp + 1) * pNN; }
+  __host__ __device__ static int oT(int rp) { return oP(rp) + (rp + 2) * VS; }
+  __host__ __device__ static int oU(int rp) { return oT(rp) + (rp + 2) * VS; }
+  __host__ __device__ static int oRed(int rp) { return oU(rp) + rp * VS; }
+  __host__ __device__ static int oVals(int rp) { return oRed(rp) + 32; }
+  __host__ __device__ static int total(int rp) { return oVals(rp) + 160; }
+};
+
+// LL ("low-latency") words, as in NCCL's LL protocol: every 8-byte word
+// carries 32 bits of payload and a 32-bit epoch flag, written and read as one
+// single-copy-atomic access, so a reader that sees the expected flag has the
+// payload — no fences, no separate flag round trip. A value of T occupies one
+// 16-byte slot: {lo32 | flag, hi32 | flag}.
+__device__ __forceinline__ void ll_store(unsigned long long* p, double v, unsigned flag) {
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+  const unsigned long long f = static_cast<unsigned long long>(flag) << 32;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(f | (bits & 0xffffffffull)),
+               "l"(f | (bits >> 32))
+               : "memory");
+}
+__device__ __forceinline__ void ll_store(unsigned long long* p, float v, unsigned flag) {
+  const unsigned long long f = static_cast<unsigned long long>(flag) << 32;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p),
+               "l"(f | static_cast<unsigned long long>(__float_as_uint(v))), "l"(f)
+               : "memory");
+}
+constexpr int kSlotU64 = 16;  // reduction slot stride: 128 bytes
+constexpr int kMaxPoll = 5;   // slots per lane: G <= 160
+
+__device__ __forceinline__ void ll_ld2(const unsigned long long* p, unsigned long long& a,
+                                       unsigned long long& b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+template <class T>
+__device__ __forceinline__ T ll_value(unsigned long long a, unsigned long long b) {
+  if constexpr (sizeof(T) == 8)
+    return __longlong_as_double(static_cast<long long>((b << 32) | (a & 0xffffffffull)));
+  else
+    return __uint_as_float(static_cast<unsigned>(a));
+}
+// Lane-parallel gather of the G reduction slots (slot j -> lane j % 32,
+// register j / 32): every lane issues all its loads at once and re-polls only
+// the slots whose flag is not there yet. Lanes with no slot get slot 0.
+template <class T>
+__device__ __forceinline__ void ll_gather(const unsigned long long* slots, int G, unsigned epoch,
+                                          int lane, T (&out)[kMaxPoll]) {
+  unsigned long long a[kMaxPoll], b[kMaxPoll];
+#pragma unroll
+  for (int k = 0; k < kMaxPoll; ++k) {
+    const int j = lane + 32 * k < G ? lane + 32 * k : 0;
+    ll_ld2(slots + kSlotU64 * j, a[k], b[k]);
+  }
+  bool done;
+  do {
+    done = true;
+#pragma unroll
+    for (int k = 0; k < kMaxPoll; ++k) {
+      if (static_cast<unsigned>(a[k] >> 32) != epoch || static_cast<unsigned>(b[k] >> 32) != epoch) {
+        done = false;
+        const int j = lane + 32 * k < G ? lane + 32 * k : 0;
+        ll_ld2(slots + kSlotU64 * j, a[k], b[k]);
+      }
+    }
+  } while (!done);
+#pragma unroll
+  for (int k = 0; k < kMaxPoll; ++k) out[k] = ll_value<T>(a[k], b[k]);
+}
+
+template <class T>
+__device__ __forceinline__ T ll_load(const unsigned long long* p, unsigned flag) {
+  unsigned long long a, b;
+  do {
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  } while (static_cast<unsigned>(a >> 32) != flag || static_cast<unsigned>(b >> 32) != flag);
+  if constexpr (sizeof(T) == 8)
+    return __longlong_as_double(static_cast<long long>((b << 32) | (a & 0xffffffffull)));
+  else
+    return __uint_as_float(static_cast<unsigned>(a));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_g2s(void* dst, const void* src, unsigned bytes, unsigned mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, "
+        "p;\n}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(phase)
+        : "memory");
+  }
+}
+
+struct Piece {
+  void* dst;
+  const void* src;
+  unsigned bytes;
+};
+// Stage up to 4 global ranges into the warp's tile: TMA bulk copies for the
+// 16-byte aligned ones (completed on the warp's mbarrier), lane copies for
+// the rest. Every lane returns with the data visible.
+template <class T>
+__device__ __forceinline__ void warp_stage(const Piece (&pc)[4], int n, unsigned mbar,
+                                           unsigned& phase, int lane) {
+  unsigned tx = 0;
+  bool ok[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ok[i] = i < n && pc[i].bytes > 0 &&
+            ((reinterpret_cast<uintptr_t>(pc[i].src) | reinterpret_cast<uintptr_t>(pc[i].dst) |
+              pc[i].bytes) & 15u) == 0;
+    if (ok[i]) tx += pc[i].bytes;
+  }
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    mbar_expect(mbar, tx);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (ok[i]) tma_g2s(pc[i].dst, pc[i].src, pc[i].bytes, mbar);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < n && !ok[i]) {
+      const int cnt = static_cast<int>(pc[i].bytes / sizeof(T));
+      for (int j = lane; j < cnt; j += 32)
+        static_cast<T*>(pc[i].dst)[j] = static_cast<const T*>(pc[i].src)[j];
+    }
+  }
+  mbar_wait(mbar, phase);
+  phase ^= 1u;
+  __syncwarp();
+}
+
+}  // namespace
+
+// Row l of A_k Q_k^-1 (At, Qk: row-major tiles in shared memory): the q loop
+// stays rolled (one broadcast row of Q_k^-1 per step) so the n = 28 code fits
+// the instruction cache; explicit fma keeps the owner's L_lo and the
+// neighbour's recomputed L_hi bitwise equal.
+template <class T, int NB>
+__device__ __forceinline__ void row_aq(const T* At, const T* Qk, int lr, T (&aq)[NB]) {
+#pragma unroll
+  for (int j = 0; j < NB; ++j) aq[j] = T(0);
+#pragma unroll 1
+  for (int q = 0; q < NB; ++q) {
+    const T a = At[lr * NB + q];
+#pragma unroll
+    for (int j = 0; j < NB; j += 2) {
+      const auto v = ld2<T>(Qk + q * NB + j);
+      aq[j] = fma(a, v.x, aq[j]);
+      aq[j + 1] = fma(a, v.y, aq[j + 1]);
+    }
+  }
+}
+
+// kMaxRp: most block rows per CTA this instantiation supports (launch bound)
+template <class T, int NB> struct FgMaxRp { static constexpr int v = NB > 16 ? 4 : 7; };
+
+template <class T, int NB, int MB>
+__global__ void __launch_bounds__(32 * (FgMaxRp<T, NB>::v + 1), 1)
+    k_fg(FusedParams<T> p, FgSync<T> sy, int rp) {
+  using FL = FgLayout<T, NB, MB>;
+  constexpr int NN = FL::NN, MM = FL::MM, NM = FL::NM, VS = FL::VS;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int K = p.K, N = K - 1;
+  const int lo = c * rp, hi = min(K, lo + rp), nrow = hi - lo;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  const bool xw = (w == rp);  // the extra (halo-knot) warp
+  const bool rowv = w < nrow;
+  const int b = lo + (rowv ? w : 0);
+  const int l = lane;
+  const bool lact = l < NB;
+  const int lr = lact ? l : NB - 1;
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* tileW = sm + FL::tile(w);
+  T* sD = sm + FL::oD(rp);
+  T* sL = sm + FL::oL(rp);  // L_lo .. L_hi
+  T* sP = sm + FL::oP(rp);  // p rows lo-1 .. hi
+  T* sT = sm + FL::oT(rp);  // t rows lo-1 .. hi
+  T* sU = sm + FL::oU(rp);
+  T* red = sm + FL::oRed(rp);
+  T* vals = sm + FL::oVals(rp);
+  __shared__ __align__(8) unsigned long long s_mbar[9];
+  __shared__ int s_err;
+  const unsigned mbar = static_cast<unsigned>(__cvta_generic_to_shared(&s_mbar[w]));
+  unsigned mphase = 0;
+  if (lane == 0) mbar_init(mbar);
+  __syncthreads();
+
+  // epoch counters (lockstep in every CTA; the host offsets them per launch so
+  // stale words of earlier launches never match)
+  unsigned rb = sy.epoch0, tx = sy.epoch0, xe = sy.epoch0;
+  // fixed-order all-reduce over the grid (op 0: sum, 1: min): warp trees, the
+  // CTA's warp partials in warp order, then warp 0 of every CTA reads the G
+  // LL slots and combines them in one fixed order -> bit-identical in all CTAs
+  auto combine = [](T a, T b, int op) -> T { return op ? (b < a ? b : a) : a + b; };
+  auto allreduce = [&](T v, int op) -> T {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = combine(v, __shfl_xor_sync(FULL, v, o), op);
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    const int buf = static_cast<int>(rb & 1u);
+    const unsigned epoch = ++rb;
+    if (w == 0) {
+      T cv = red[0];
+      for (int i = 1; i < nw; ++i) cv = combine(cv, red[i], op);
+      T acc = cv;
+      if (G > 1) {
+        // one 128-byte line per CTA slot: the polls of G warps spread over
+        // many L2 lines instead of queueing on a few
+        unsigned long long* slots = sy.red + static_cast<size_t>(buf) * sy.gstride * kSlotU64;
+        if (lane == 0) ll_store(slots + kSlotU64 * c, cv, epoch);
+        T got[kMaxPoll];
+        ll_gather<T>(slots, G, epoch, lane, got);
+        acc = lane < G ? got[0] : (op ? got[0] : T(0));
+#pragma unroll
+        for (int k = 1; k < kMaxPoll; ++k)
+          if (lane + 32 * k < G) acc = combine(acc, got[k], op);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = combine(acc, __shfl_xor_sync(FULL, acc, o), op);
+      }
+      if (lane == 0) vals[0] = acc;
+    }
+    __syncthreads();
+    return vals[0];
+  };
+
+  // optional per-phase globaltimer stamps of CTA 0 (B2P_PHASE_TIMING=1):
+  // [0] start [1] staged [2] F1 [3] F2 + error agreement [4] PCG init;
+  // [5] sum(Srow + upsilon) [6] sum(preconditioner incl. t exchange) [7] sum(eta' + p update)
+  auto stamp = [&]() -> unsigned long long {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  };
+  for (int sys = 0; sys < p.B; ++sys) {
+    unsigned long long* tm = (p.timing && c == 0 && tid == 0) ? p.timing + static_cast<size_t>(sys) * 8 : nullptr;
+    if (tm) {
+      tm[0] = stamp();
+      tm[5] = tm[6] = tm[7] = 0;
+    }
+    const T* Qs = p.Q + static_cast<size_t>(sys) * K * NN;
+    const T* qs = p.q + static_cast<size_t>(sys) * K * NB;
+    const T* Rs = p.R + static_cast<size_t>(sys) * N * MM;
+    const T* rs = p.r + static_cast<size_t>(sys) * N * MB;
+    const T* As = p.A + static_cast<size_t>(sys) * N * NN;
+    const T* Bs = p.Bm + static_cast<size_t>(sys) * N * NM;
+    const T* es = p.e + static_cast<size_t>(sys) * N * NB;
+    const T* xs = p.x_s + static_cast<size_t>(sys) * NB;
+    const T* x0 = p.x0 + static_cast<size_t>(sys) * NB;
+    if (tid == 0) s_err = INT_MAX;
+    int fkey = INT_MAX;
+    __syncthreads();
+
+    // ====================================================== stage inputs
+    // warp w < nrow: knot b (Q_b, R_b) and row b's A_{b-1}, B_{b-1};
+    // extra warp: knot lo-1 (Q, R) and A_{hi-1} (for L_hi).
+    int kw = -1;  // knot whose Q, R this warp inverts
+    {
+      Piece pc[4];
+      int n = 0;
+      if (rowv) {
+        kw = b;
+        pc[n++] = {tileW + FL::oQt, Qs + static_cast<size_t>(kw) * NN, unsigned(sizeof(T) * NN)};
+        if (kw < N) pc[n++] = {tileW + FL::oRt, Rs + static_cast<size_t>(kw) * MM, unsigned(sizeof(T) * MM)};
+        if (b > 0) {
+          pc[n++] = {tileW + FL::oAt, As + static_cast<size_t>(b - 1) * NN, unsigned(sizeof(T) * NN)};
+          pc[n++] = {tileW + FL::oBt, Bs + static_cast<size_t>(b - 1) * NM, unsigned(sizeof(T) * NM)};
+        }
+      } else if (xw) {
+        if (lo > 0) {
+          kw = lo - 1;
+          pc[n++] = {tileW + FL::oQt, Qs + static_cast<size_t>(kw) * NN, unsigned(sizeof(T) * NN)};
+          pc[n++] = {tileW + FL::oRt, Rs + static_cast<size_t>(kw) * MM, unsigned(sizeof(T) * MM)};
+        }
+        if (hi < K)
+          pc[n++] = {tileW + FL::oAt, As + static_cast<size_t>(hi - 1) * NN, unsigned(sizeof(T) * NN)};
+      }
+      if (rowv || xw) warp_stage<T>(pc, n, mbar, mphase, lane);
+    }
+    if (tm) tm[1] = stamp();
+    T* Lr = tileW + FL::oLr;
+    T* Li = tileW + FL::oLi;
+    T* rd = tileW + FL::ord;
+
+    // ====================================================== F1: knot kw
+    // Q_kw^-1 (in place), Q^-1 q, R_kw^-1 (in place), R^-1 r (schur.cpp:15-23)
+    if (kw >= 0) {
+      T* Qt = tileW + FL::oQt;
+      T a[NB], x[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) a[i] = Qt[lr * NB + i];
+      const int f = wp_spd_inverse<T, NB>(a, Lr, Li, rd, l, x);
+      if (rowv && f >= 0) fkey = min(fkey, kw == 0 ? 0 : 4 * kw + 2);
+      if (lact) {
+        T qq = T(0);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          Qt[l * NB + i] = x[i];
+          qq += x[i] * qs[static_cast<size_t>(kw) * NB + i];
+        }
+        tileW[FL::oqq + l] = qq;
+      }
+      __syncwarp();
+      if (kw < N) {
+        T* Rt = tileW + FL::oRt;
+        T ra[MB], y[MB];
+        const int lm = l < MB ? l : MB - 1;
+#pragma unroll
+        for (int i = 0; i < MB; ++i) ra[i] = Rt[lm * MB + i];
+        const int g = wp_spd_inverse<T, MB>(ra, Lr, Li, rd, l, y);
+        if (rowv && g >= 0) fkey = min(fkey, 4 * (kw + 1) + 1);
+        if (l < MB) {
+          T rr = T(0);
+#pragma unroll
+          for (int i = 0; i < MB; ++i) {
+            Rt[l * MB + i] = y[i];
+            rr += y[i] * rs[static_cast<size_t>(kw) * MB + i];
+          }
+          tileW[FL::orr + l] = rr;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();  // every knot tile of the CTA is final
+    if (tm) tm[2] = stamp();
+
+    // ====================================================== F2: row b
+    T ti[NB], lrow[NB];
+    T gam = T(0);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) ti[i] = lrow[i] = T(0);
+    if (rowv) {
+      const T* Qb = tileW + FL::oQt;  // Q_b^-1 (own knot)
+      if (b == 0) {
+        // schur.cpp:53-57: S(0,0) = Q0^-1, theta_inv[0] = sym(Q0), gamma_0
+        if (lact) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            sD[l * NB + i] = Qb[l * NB + i];
+            ti[i] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
+          }
+          gam = -((xs[l] - x0[l]) + tileW[FL::oqq + l]);
+        }
+      } else {
+        const int k = b - 1;
+        const T* kt = sm + FL::tile(w > 0 ? w - 1 : rp);  // knot k's tile
+        const T* Qk = kt + FL::oQt;
+        const T* Rk = kt + FL::oRt;
+        const T* At = tileW + FL::oAt;
+        const T* Bt = tileW + FL::oBt;
+        // AQ = A_k Q_k^-1 (row l); L_b = phi = -AQ (schur.cpp:68)
+        T aq[NB];
+        row_aq<T, NB>(At, Qk, lr, aq);
+        T* Lb = sL + w * FL::pNN;
+        if (lact) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) Lb[l * NB + j] = -aq[j];
+        }
+        // BR = B_k R_k^-1 (row l)
+        T br[MB];
+#pragma unroll
+        for (int q = 0; q < MB; ++q) br[q] = T(0);
+#pragma unroll 1
+        for (int s = 0; s < MB; ++s) {
+          const T bv = Bt[lr * MB + s];
+#pragma unroll
+          for (int q = 0; q < MB; ++q) br[q] = fma(bv, Rk[s * MB + q], br[q]);
+        }
+        // theta_raw row l = (AQ A')(l,:) + (BR B')(l,:) + Q_b^-1(l,:)  (schur.cpp:65-66),
+        // written straight into the Lr tile (rolled over i)
+#pragma unroll 1
+        for (int i = 0; i < NB; ++i) {
+          T s1 = T(0), s2 = T(0);
+#pragma unroll
+          for (int q = 0; q < NB; q += 2) {
+            const auto v = ld2<T>(At + i * NB + q);
+            s1 = fma(aq[q], v.x, s1);
+            s1 = fma(aq[q + 1], v.y, s1);
+          }
+#pragma unroll
+          for (int q = 0; q < MB; ++q) s2 = fma(br[q], Bt[i * MB + q], s2);
+          if (lact) Lr[l * NB + i] = (s1 + s2) + Qb[l * NB + i];
+        }
+        // zeta = -A (Q_k^-1 q_k) - B (R_k^-1 r_k) + Q_b^-1 q_b; gamma (schur.cpp:69-77)
+        {
+          T aqq = T(0), brr = T(0);
+#pragma unroll 1
+          for (int q = 0; q < NB; ++q) aqq = fma(At[lr * NB + q], kt[FL::oqq + q], aqq);
+#pragma unroll 1
+          for (int q = 0; q < MB; ++q) brr = fma(Bt[lr * MB + q], kt[FL::orr + q], brr);
+          const T zeta = (-aqq - brr) + tileW[FL::oqq + lr];
+          gam = -(-es[static_cast<size_t>(k) * NB + lr] + zeta);
+        }
+        // theta = 0.5 (theta_raw + theta_raw') (schur.cpp:67)
+        __syncwarp();
+        T th[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) th[i] = T(0.5) * (Lr[lr * NB + i] + Lr[i * NB + lr]);
+        __syncwarp();
+        if (lact) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) sD[w * FL::pNN + l * NB + i] = th[i];
+        }
+        // theta^-1 (schur.cpp:75)
+        const int f = wp_spd_inverse<T, NB>(th, Lr, Li, rd, l, ti);
+        if (f >= 0) fkey = min(fkey, b * 4 + 3);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < NB; ++j) lrow[j] = Lb[lr * NB + j];
+      }
+    } else if (xw && hi < K) {
+      // L_hi = -A_{hi-1} Q_{hi-1}^-1: the next CTA's first L block, same arithmetic
+      const T* Qk = sm + FL::tile(nrow - 1) + FL::oQt;
+      const T* At = tileW + FL::oAt;
+      T aq[NB];
+      row_aq<T, NB>(At, Qk, lr, aq);
+      if (lact) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) sL[nrow * FL::pNN + l * NB + j] = -aq[j];
+      }
+    }
+    if (lane == 0 && rowv && fkey != INT_MAX) atomicMin(&s_err, fkey);
+    __syncthreads();
+    {
+      // first failing call in row order over the whole system (grid min; the
+      // keys are small integers, exact in T)
+      const T ek = allreduce(s_err == INT_MAX ? T(1e30) : static_cast<T>(s_err), 1);
+      if (ek < T(1e29)) {
+        if (c == 0 && tid == 0) {
+          p.errkey[sys] = static_cast<int>(ek);
+          SysOut o{};
+          o.code = kRuntime;
+          o.which = kWhichNone;
+          o.iteration = -1;
+          p.out[sys] = o;
+        }
+        continue;
+      }
+    }
+    if (c == 0 && tid == 0) p.errkey[sys] = 0x7f7f7f7f;
+    if (tm) tm[3] = stamp();
+
+    // ====================================================== P
+    const bool hasL = rowv && b > 0;
+    const bool hasR = rowv && b + 1 < K;
+    const bool act = rowv && lact;
+    const T* Dw = sD + w * FL::pNN + lr * NB;
+    const T* Lcol = sL + (w + 1) * FL::pNN + lr;  // column l of L_{b+1}
+    T* myP = sP + (w + 1) * VS;
+
+    auto Srow = [&]() -> T {  // ((D p_b + L p_{b-1}) + R p_{b+1}), block_tri.cpp:82-92
+      T out = dot_row<T, NB>(Dw, myP);
+      if (hasL) out += dot_reg<T, NB>(lrow, myP - VS);
+      if (hasR) out += dot_col<T, NB>(Lcol, myP + VS);
+      return out;
+    };
+    const bool stairish = p.kind == kStair || p.kind == kSymStair;
+    // r~ = Phi^-1 r for every kind; the stair family on the fly:
+    // t = theta^-1 r, u = r - L t_{b-1} - R t_{b+1}, r~ = theta^-1 u
+    auto precondition = [&](T rv) -> T {
+      if (p.kind == kIdentity) return rv;
+      if (act) sU[w * VS + l] = rv;
+      __syncwarp();
+      const T tv = dot_reg<T, NB>(ti, sU + w * VS);
+      if (!stairish) return tv;
+      if (act) sT[(w + 1) * VS + l] = tv;
+      if (G > 1) {
+        // boundary rows of t to the neighbours (LL words), then theirs back
+        const unsigned ep = ++tx;
+        if (act && w == 0) ll_store(sy.xt + ((static_cast<size_t>(c) * 2 + 0) * VS + l) * 2, tv, ep);
+        if (act && w == nrow - 1) ll_store(sy.xt + ((static_cast<size_t>(c) * 2 + 1) * VS + l) * 2, tv, ep);
+        if (w == 0 && lo > 0 && lact)
+          sT[l] = ll_load<T>(sy.xt + ((static_cast<size_t>(c - 1) * 2 + 1) * VS + l) * 2, ep);
+        if (xw && hi < K && lact)
+          sT[(nrow + 1) * VS + l] = ll_load<T>(sy.xt + ((static_cast<size_t>(c + 1) * 2) * VS + l) * 2, ep);
+      }
+      __syncthreads();
+      T uv = rv;
+      if (hasL) uv -= dot_reg<T, NB>(lrow, sT + w * VS);
+      if (hasR) uv -= dot_col<T, NB>(Lcol, sT + (w + 2) * VS);
+      __syncwarp();
+      if (act) sU[w * VS + l] = uv;
+      __syncwarp();
+      const bool corr = (p.kind == kSymStair) || (b & 1);
+      return corr ? dot_reg<T, NB>(ti, sU + w * VS) : tv;
+    };
+    // publish the boundary rows of r~ (read by the neighbours after the eta reduction)
+    auto publish_rt = [&](T rt) {
+      ++xe;
+      if (G > 1 && act) {
+        if (w == 0) ll_store(sy.xr + ((static_cast<size_t>(c) * 2 + 0) * VS + l) * 2, rt, xe);
+        if (w == nrow - 1) ll_store(sy.xr + ((static_cast<size_t>(c) * 2 + 1) * VS + l) * 2, rt, xe);
+      }
+    };
+    // p halo rows lo-1 (from CTA c-1) and hi (from CTA c+1): p = r~ + beta p
+    auto halo_p = [&](bool first, T beta) {
+      if (w == 0 && lo > 0 && lact) {
+        const T rn = ll_load<T>(sy.xr + ((static_cast<size_t>(c - 1) * 2 + 1) * VS + l) * 2, xe);
+        sP[l] = first ? rn : fma(beta, sP[l], rn);
+      }
+      if (xw && hi < K && lact) {
+        const T rn = ll_load<T>(sy.xr + ((static_cast<size_t>(c + 1) * 2) * VS + l) * 2, xe);
+        T* ph = sP + (nrow + 1) * VS;
+        ph[l] = first ? rn : fma(beta, ph[l], rn);
+      }
+    };
+
+    // r = gamma - S lambda0 (pcg.cpp:62)
+    const size_t voff = static_cast<size_t>(sys) * K * NB;
+    T lam = T(0);
+    if (p.lambda0) {
+      for (int i = tid; i < (nrow + 2) * VS; i += blockDim.x) {
+        const int row = lo - 1 + i / VS, j = i % VS;
+        sP[i] = (row >= 0 && row < K && j < NB) ? p.lambda0[voff + static_cast<size_t>(row) * NB + j] : T(0);
+      }
+      __syncthreads();
+      if (act) lam = myP[l];
+    }
+    T rr = act ? gam - (p.lambda0 ? Srow() : T(0)) : T(0);
+    __syncthreads();
+    T rt = precondition(rr);
+    if (!act) rt = T(0);
+    publish_rt(rt);
+    T eta = allreduce(act ? rr * rt : T(0), 0);
+    T pp = rt;
+    if (act) myP[l] = pp;
+    halo_p(true, T(0));
+    __syncthreads();
+    unsigned long long t0 = 0;
+    if (tm) tm[4] = t0 = stamp();
+
+    int code = kOk, which = kWhichNone, err_iter = -1, iterations = 0, converged = 0;
+    double exit_eta = static_cast<double>(eta), value = 0.0;
+    T best_eta = eta, best = lam;
+    double* trace = p.trace ? p.trace + static_cast<size_t>(sys) * p.trace_cap : nullptr;
+    if (!is_finite(eta)) {
+      code = kRuntime;
+      which = kWhichInitNonFinite;
+    } else if (static_cast<double>(eta) < p.epsilon) {
+      converged = 1;
+    } else {
+      for (int it = 1; it <= p.max_iter; ++it) {
+        const T spv = rowv ? Srow() : T(0);
+        const T ups = allreduce(act ? pp * spv : T(0), 0);
+        if (!is_finite(ups)) {
+          code = kRuntime;
+          which = kWhichUpsNonFinite;
+          err_iter = it;
+          break;
+        }
+        if (ups <= T(0)) {
+          code = kBreakdown;
+          which = kWhichBreakdown;
+          err_iter = it;
+          value = static_cast<double>(ups);
+          break;
+        }
+        const T alpha = eta / ups;
+        rr -= alpha * spv;
+        lam += alpha * pp;
+        if (tm) { const unsigned long long t1 = stamp(); tm[5] += t1 - t0; t0 = t1; }
+        rt = precondition(rr);
+        if (!act) rt = T(0);
+        publish_rt(rt);
+        if (tm) { const unsigned long long t1 = stamp(); tm[6] += t1 - t0; t0 = t1; }
+        const T eta_p = allreduce(act ? rr * rt : T(0), 0);
+        if (!is_finite(eta_p)) {
+          code = kRuntime;
+          which = kWhichEtaNonFinite;
+          err_iter = it;
+          break;
+        }
+        if (trace && c == 0 && tid == 0) trace[it - 1] = static_cast<double>(eta_p);
+        if (eta_p < best_eta) {
+          best_eta = eta_p;
+          best = lam;
+        }
+        iterations = it;
+        exit_eta = static_cast<double>(eta_p);
+        if (static_cast<double>(eta_p) < p.epsilon) {
+          converged = 1;
+          break;
+        }
+        if (it == p.max_iter) break;
+        const T beta = eta_p / eta;
+        pp = fma(beta, pp, rt);
+        if (act) myP[l] = pp;
+        halo_p(false, beta);
+        eta = eta_p;
+        __syncthreads();
+        if (tm) { const unsigned long long t1 = stamp(); tm[7] += t1 - t0; t0 = t1; }
+      }
+    }
+    if (code == kOk && act)
+      p.lambda_out[voff + static_cast<size_t>(b) * NB + l] = converged ? lam : best;
+    if (c == 0 && tid == 0) {
+      SysOut o;
+      o.code = code;
+      o.knot = -1;
+      o.which = which;
+      o.iteration = err_iter;
+      o.iterations = iterations;
+      o.converged = converged;
+      o.exit_eta = exit_eta;
+      o.value = value;
+      o.max_drift = 0.0;
+      o.trace_len = (trace && code == kOk) ? iterations : 0;
+      o._pad = 0;
+      p.out[sys] = o;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+template <class T, int NB, int MB>
+size_t fg_smem(int rp) {
+  return sizeof(T) * static_cast<size_t>(FgLayout<T, NB, MB>::total(rp));
+}
+template <class T>
+bool fg_shape(int n, int m) {
+  if (sizeof(T) == 8) return (n == 28 && m == 14) || (n == 14 && m == 7);
+  return n == 12 && m == 4;
+}
+template <class T>
+size_t fg_smem_rt(int n, int m, int rp) {
+  if (sizeof(T) == 8) return n == 28 ? fg_smem<T, 28, 14>(rp) : fg_smem<T, 14, 7>(rp);
+  return fg_smem<T, 12, 4>(rp);
+}
+}  // namespace
+
+template <class T>
+int fg_pick_rp(int K, int n, int m, int kind, int sm_count, int want_rp) {
+  if (!fg_shape<T>(n, m) || kind == kPoly || K < 2) return 0;
+  const size_t budget = 227 * 1024 - 1024;
+  auto ok = [&](int rp) {
+    const int G = (K + rp - 1) / rp;
+    const int maxrp = (n > 16) ? FgMaxRp<T, 32>::v : FgMaxRp<T, 16>::v;
+    return rp >= 1 && rp <= maxrp && G <= sm_count && (K + rp - 1) / rp * rp - K < rp &&
+           fg_smem_rt<T>(n, m, rp) <= budget;
+  };
+  if (want_rp > 0) return ok(want_rp) ? want_rp : 0;
+  // 4 rows per CTA where the grid allows it (measured best for c2 / c5: fewer,
+  // fuller CTAs make the grid reductions cheaper), else the fewest rows per
+  // CTA that keep every CTA of the grid co-resident
+  for (int rp = 4; rp <= 8; ++rp)
+    if (ok(rp)) return rp;
+  for (int rp = 1; rp < 4; ++rp)
+    if (ok(rp)) return rp;
+  return 0;
+}
+
+template <class T>
+cudaError_t launch_fg(const FusedParams<T>& p, const FgSync<T>& sy, int rp, cudaStream_t st) {
+  const int G = (p.K + rp - 1) / rp;
+  auto go = [&](auto kern, size_t smem) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    FusedParams<T> pp = p;
+    FgSync<T> ss = sy;
+    int r = rp;
+    void* args[] = {&pp, &ss, &r};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(G), dim3(32 * (rp + 1)),
+                                       args, smem, st);
+  };
+  if constexpr (sizeof(T) == 8) {
+    if (sy.n == 28) return go(k_fg<T, 28, 14>, fg_smem<T, 28, 14>(rp));
+    return go(k_fg<T, 14, 7>, fg_smem<T, 14, 7>(rp));
+  } else {
+    return go(k_fg<T, 12, 4>, fg_smem<T, 12, 4>(rp));
+  }
+}
+
+template int fg_pick_rp<double>(int, int, int, int, int, int);
+template int fg_pick_rp<float>(int, int, int, int, int, int);
+template cudaError_t launch_fg<double>(const FusedParams<double>&, const FgSync<double>&, int,
+                                       cudaStream_t);
+template cudaError_t launch_fg<float>(const FusedParams<float>&, const FgSync<float>&, int,
+                                      cudaStream_t);
+
+}  // namespace b2p

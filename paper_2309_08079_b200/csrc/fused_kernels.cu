@@ -57,6 +57,33 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// One-thread TMA bulk copy global -> shared, completed on an mbarrier
+// (16-byte aligned source, destination and size).
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, unsigned bytes,
+                                            unsigned mbar_addr) {
+  asm volatile("fence.proxy.async;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst_smem))),
+      "l"(src), "r"(bytes), "r"(mbar_addr)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned mbar_addr, unsigned& phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
+        "1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(mbar_addr), "r"(phase)
+        : "memory");
+  }
+  phase ^= 1u;
+}
+
 template <class T, int NB, int MB, int R>
 __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -125,16 +152,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // ============================================================ F1: knots
     // Q_k^-1 for every knot and R_k^-1 for k < N, computed once and shared
     // by the two block rows that use them (the reference recomputes them per
-    // row, schur.cpp:49-51; same arithmetic).
+    // row, schur.cpp:49-51; same arithmetic). All Q_k arrive in one TMA bulk
+    // copy (sQi) and are inverted in place; lanes read their rows from smem.
+    if (tid == 0) tma_load_1d(sQi, Qs, static_cast<unsigned>(sizeof(T) * K * nn), mbar_addr);
+    mbar_wait(mbar_addr, mbar_phase);
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
       const int k = h + r * kHalfWarps;
       if (k < K) {
         T a[NB], x[NB];
-        const T* Qr = Qs + static_cast<size_t>(k) * nn + lr * NB;
+        const T* Qr = sQi + static_cast<size_t>(k) * nn + lr * NB;
 #pragma unroll
-        for (int i = 0; i < NB; ++i) a[i] = Qr[i];
+        for (int i = 0; i < NB; i += 2) {
+          const double2 q2 = *reinterpret_cast<const double2*>(Qr + i);
+          a[i] = q2.x;
+          a[i + 1] = q2.y;
+        }
         const int f = hw_spd_inverse_v2<T, NB>(a, tW, tX, rd, l, x);
+        __syncwarp(hw_mask());  // every lane has consumed its Q_k row: overwrite in place
         // first failing call in row order: row k as its Q_{k+1} (key 4k+2), or row 0
         if (f >= 0) fkey = min(fkey, k == 0 ? 0 : 4 * k + 2);
         if (lact) {
@@ -299,17 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // KKT inputs into L2 so its formation phase does not start on cold HBM.
     {
       const unsigned bytes = static_cast<unsigned>(sizeof(T) * 2 * K * NN);
-      if (tid == 0) {
-        asm volatile("fence.proxy.async;\n" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
-                     "r"(bytes)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-            "[%3];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(sL))),
-            "l"(gL), "r"(bytes), "r"(mbar_addr)
-            : "memory");
-      }
+      if (tid == 0) tma_load_1d(sL, gL, bytes, mbar_addr);
       const int nsys = sys + gridDim.x;
       if (nsys < p.B && tid < 9) {
         // per-field contiguous ranges of the next system (16-byte aligned inside)
@@ -346,18 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
                                      : T(0);
       if (act[r]) sp[b * NB + l] = lam[r];
     }
-    {
-      unsigned done = 0;
-      while (!done) {
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
-            "1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(mbar_addr), "r"(mbar_phase)
-            : "memory");
-      }
-      mbar_phase ^= 1u;
-    }
+    mbar_wait(mbar_addr, mbar_phase);
     __syncthreads();
 
     int bc[R];  // clamped block row per owned row

@@ -88,6 +88,22 @@ template <class T> size_t fc_slot_elems(int K, int n, int G);
 template <class T>
 cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStream_t st);
 
+// Fused grid kernel (fg_kernels.cu): one long-horizon system on G co-resident
+// CTAs (cooperative launch) of rp block rows each. FgSync is the zeroed global
+// workspace for its reduce-barriers and boundary-row exchanges.
+template <class T>
+struct FgSync {
+  unsigned long long* red;  // [2][gstride] 128-byte-strided LL slots: per-CTA reduction partials
+  unsigned long long* xt;   // [gstride][2][VS] LL slots: boundary rows of t
+  unsigned long long* xr;   // [gstride][2][VS] LL slots: boundary rows of r~
+  int gstride;
+  int n;
+  unsigned epoch0;  // first epoch of this launch (flags of older launches never match)
+};
+template <class T> int fg_pick_rp(int K, int n, int m, int kind, int sm_count, int want_rp);
+template <class T>
+cudaError_t launch_fg(const FusedParams<T>& p, const FgSync<T>& sy, int rp, cudaStream_t st);
+
 // Shared-memory footprint of one PCG CTA (bytes) for a parameter block.
 template <class T>
 size_t pcg_smem_bytes(const PcgParams<T>& p);

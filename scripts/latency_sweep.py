@@ -45,7 +45,7 @@ def timed(kkt, kind, eps, dtype=np.float64, env=None):
         orc_res = orc.solve(kkt, kind, 1, cfg, dtype=dtype)
         cpu_us = (time.perf_counter() - t0) * 1e6
         ctx = api.context()
-        path = {0: "split K1+K3", 1: "fused one-CTA", 2: "fused cluster"}[ctx.last_path()]
+        path = {0: "split K1+K3", 1: "fused one-CTA", 2: "fused cluster", 3: "fused grid"}[ctx.last_path()]
         k1_ms, k3_ms = ctx.last_phase_ms()
         return {"us_median": statistics.median(ts), "us_min": min(ts),
                 "iterations": res.report.iterations,
@@ -74,6 +74,9 @@ def main():
                                            env={"B2P_FC": "0"})
     out["c1_symstair_1e-8_cluster2"] = timed(k1, PrecondKind.symmetric_stair, 1e-8,
                                              env={"B2P_FC_G": "2"})
+    for rp in (1, 2):
+        out[f"c1_symstair_1e-8_fusedgrid_rp{rp}"] = timed(
+            k1, PrecondKind.symmetric_stair, 1e-8, env={"B2P_FG": "1", "B2P_FG_RP": str(rp)})
     k2 = orc.random_kkt(2, 127, 14, 7)
     for kind, name in [(PrecondKind.block_jacobi, "jacobi"), (PrecondKind.stair, "stair"),
                        (PrecondKind.symmetric_stair, "symstair")]:
@@ -81,6 +84,9 @@ def main():
             out[f"c2_{name}_{eps:g}"] = timed(k2, kind, eps)
     out["c2_symstair_1e-8_cluster8"] = timed(k2, PrecondKind.symmetric_stair, 1e-8,
                                              env={"B2P_FC_G": "8"})
+    for rp in (1, 2, 4):
+        out[f"c2_symstair_1e-8_fusedgrid_rp{rp}"] = timed(
+            k2, PrecondKind.symmetric_stair, 1e-8, env={"B2P_FG": "1", "B2P_FG_RP": str(rp)})
     out["c2_symstair_1e-8_split"] = timed(k2, PrecondKind.symmetric_stair, 1e-8,
                                           env={"B2P_FC": "0"})
     k3 = orc.random_kkt(3, 255, 12, 4)
@@ -90,6 +96,10 @@ def main():
     for G in (8, 16):
         out[f"c3_fp32_symstair_1e-4_fusedcluster{G}"] = timed(
             k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32, env={"B2P_FC_G": str(G)})
+    for rp in (2, 4, 7):
+        out[f"c3_fp32_symstair_1e-4_fusedgrid_rp{rp}"] = timed(
+            k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32,
+            env={"B2P_FG": "1", "B2P_FG_RP": str(rp)})
     for G in (2, 4, 8):
         out[f"c3_fp32_symstair_1e-4_split_cluster{G}"] = timed(
             k3, PrecondKind.symmetric_stair, 1e-4, dtype=np.float32,
@@ -100,6 +110,11 @@ def main():
             env={"B2P_FC": "0", "B2P_PCG_G": str(G)})
     k5 = orc.random_kkt(5, 511, 28, 14)
     out["c5_symstair_1e-8"] = timed(k5, PrecondKind.symmetric_stair, 1e-8)
+    for rp in (2, 3):
+        out[f"c5_symstair_1e-8_fusedgrid_rp{rp}"] = timed(
+            k5, PrecondKind.symmetric_stair, 1e-8, env={"B2P_FG_RP": str(rp)})
+    out["c5_symstair_1e-8_split"] = timed(k5, PrecondKind.symmetric_stair, 1e-8,
+                                          env={"B2P_FG": "0"})
     sweep = {}
     for floor in (1.0, 0.1, 0.01, 0.001):
         for coupling in (0.5, 1.0, 2.0):

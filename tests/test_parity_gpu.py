@@ -226,7 +226,8 @@ def test_cluster_kernel_cluster_sizes(api, orc, env, G, kind):
 
 
 @pytest.mark.parametrize("K", [2, 3, 17, 32, 33, 100])
-def test_cluster_kernel_ragged_horizons(api, orc, K):
+def test_cluster_kernel_ragged_horizons(api, orc, env, K):
+    env["B2P_FC"] = "1"
     kkt = orc.random_kkt(60 + K, K - 1, 14, 7)
     cfg = PcgConfig(epsilon=1e-8)
     got = api.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
@@ -234,7 +235,8 @@ def test_cluster_kernel_ragged_horizons(api, orc, K):
     _cmp(got, want, TOL64, cfg.epsilon)
 
 
-def test_cluster_kernel_warm_start_and_errors(api, orc):
+def test_cluster_kernel_warm_start_and_errors(api, orc, env):
+    env["B2P_FC"] = "1"
     kkt = orc.random_kkt(71, 127, 14, 7)  # K = 128: 4-CTA cluster
     cfg = PcgConfig(epsilon=1e-8)
     want = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
