@@ -214,6 +214,21 @@ int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
                             const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
                             b2p_solve_report* reports, b2p_error* err);
 
+/* ---- reconstruct_primal (proj/include/trajopt/kkt.hpp, kkt.cpp:153-181):
+ * dz = [x_0, u_0, ..., x_N] from the multipliers, per knot
+ * dx_k = Q_k^-1 (-(q_k + lambda_k - A_k' lambda_{k+1})), du_k = R_k^-1 (-(r_k - B_k' lambda_{k+1})).
+ * Host buffers; lambda_len must equal (N+1) n (else INVALID_ARGUMENT with the
+ * reference's "reconstruct_primal: expected lambda of length D, got X");
+ * dz_out holds (N+1) n + N m values. Like the reference's LDLT solve there
+ * is no positive-definiteness error path. */
+int b2p_reconstruct_primal(b2p_ctx* ctx, int dtype, const b2p_kkt* kkt, const void* lambda,
+                           int lambda_len, void* dz_out, b2p_error* err);
+/* Batched, every pointer in device memory ([batch] leading dimension),
+ * launched on the context stream without a host synchronisation. */
+int b2p_reconstruct_primal_batched_device(b2p_ctx* ctx, int dtype, int batch,
+                                          const b2p_kkt* kkt_batch_dev, const void* lambda_dev,
+                                          void* dz_dev, b2p_error* err);
+
 /* Device time (ms) of the most recent solve kernels on this context. */
 int b2p_ctx_last_solve_ms(b2p_ctx* ctx, float* ms);
 /* Per-kernel split of the most recent fused solve: ms[0] = K1 Schur

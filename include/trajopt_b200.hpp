@@ -457,6 +457,18 @@ inline PcgResult solve(const KKTSystem& kkt, PrecondKind kind, int order, const 
   return out;
 }
 
+/// VectorXd reconstruct_primal(const KKTSystem&, const VectorXd& lambda) (kkt.hpp; kkt.cpp:153-181).
+inline Vector reconstruct_primal(const KKTSystem& kkt, const Vector& lambda) {
+  const PackedKKT p = pack(kkt);
+  const b2p_kkt v = p.view(kkt.N, kkt.n, kkt.m);
+  Vector dz(static_cast<size_t>(kkt.N + 1) * kkt.n + static_cast<size_t>(kkt.N) * kkt.m);
+  b2p_error e{};
+  detail::raise(b2p_reconstruct_primal(detail::context(), B2P_F64, &v, lambda.data(),
+                                       static_cast<int>(lambda.size()), dz.data(), &e),
+                e);
+  return dz;
+}
+
 }  // namespace trajopt_b200
 
 #if defined(__has_include)

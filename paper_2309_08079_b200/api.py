@@ -374,6 +374,29 @@ def solve_batched_device(kkt_dev: KKTSystem, lambda_out_ptr: int, batch: int,
     return [SolveReport.from_c(r) for r in reps] if want_reports else None
 
 
+def reconstruct_primal(kkt: KKTSystem, lam, dtype=np.float64) -> np.ndarray:  # kkt.cpp:153-181
+    """dz = [x_0, u_0, ..., x_N] from the multipliers (one warp per knot block)."""
+    dt = np.dtype(dtype)
+    k = kkt.astype(dt)
+    lam = np.ascontiguousarray(np.asarray(lam), dtype=dt).reshape(-1)
+    dz = np.zeros(k.primal_dim(), dtype=dt)
+    err = _abi.ErrorC()
+    _check(load().b2p_reconstruct_primal(context().handle, _dt(dt), C.byref(k.to_c()), _ptr(lam),
+                                         int(lam.size), _ptr(dz), C.byref(err)), err)
+    return dz
+
+
+def reconstruct_primal_batched_device(kkt_dev: KKTSystem, lambda_ptr: int, dz_ptr: int,
+                                      batch: int, dtype=np.float64, ctx: Context | None = None):
+    """Device-resident batch (tensors with .data_ptr()); no host sync."""
+    ctx = ctx or context()
+    kc = kkt_dev.to_c(ptr=lambda t: t.data_ptr())
+    err = _abi.ErrorC()
+    _check(load().b2p_reconstruct_primal_batched_device(ctx.handle, _dt(dtype), batch,
+                                                        C.byref(kc), lambda_ptr, dz_ptr,
+                                                        C.byref(err)), err)
+
+
 def solve_batched_multi(devices, kkt_batch: KKTSystem, kind=PrecondKind.symmetric_stair,
                         order: int = 1, cfg: PcgConfig | None = None, dtype=np.float64):
     """K4: contiguous batch-index shards, one host thread + context per device."""

@@ -1228,6 +1228,75 @@ int b2p_solve(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
   });
 }
 
+// ------------------------------------------------------------------ reconstruct_primal
+}  // extern "C"
+namespace {
+template <class T>
+void primal_impl(b2p_ctx* c, int B, const b2p_kkt* k, const KktDev& kv, const void* lam, void* dz,
+                 cudaStream_t st) {
+  PrimalParams<T> p{};
+  p.B = B;
+  p.N = k->N;
+  p.n = k->n;
+  p.m = k->m;
+  p.Q = static_cast<const T*>(kv.Q);
+  p.q = static_cast<const T*>(kv.q);
+  p.R = static_cast<const T*>(kv.R);
+  p.r = static_cast<const T*>(kv.r);
+  p.A = static_cast<const T*>(kv.A);
+  p.B_ = static_cast<const T*>(kv.B);
+  p.lambda = static_cast<const T*>(lam);
+  p.dz = static_cast<T*>(dz);
+  CK(launch_reconstruct_primal<T>(p, st));
+  c->launches++;
+}
+}  // namespace
+extern "C" {
+
+int b2p_reconstruct_primal(b2p_ctx* c, int dtype, const b2p_kkt* k, const void* lambda,
+                           int lambda_len, void* dz_out, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(k);
+    check_ctx(c);
+    const int D = (k->N + 1) * k->n;
+    if (lambda_len != D)
+      throw invalid("reconstruct_primal: expected lambda of length " + std::to_string(D) +
+                    ", got " + std::to_string(lambda_len));
+    if (!lambda || !dz_out) throw invalid("reconstruct_primal: null buffer");
+    const size_t es = esize(dtype);
+    const size_t P = static_cast<size_t>(k->N + 1) * k->n + static_cast<size_t>(k->N) * k->m;
+    cudaStream_t st = c->stream();
+    void* in = ws_get(c, "rp_in", kkt_block_bytes(k, es, 1));
+    const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st);
+    void* dl = ws_get(c, "rp_l", es * D);
+    void* dd = ws_get(c, "rp_dz", es * P);
+    h2d(c, dl, lambda, es * D, st);
+    if (dtype == B2P_F64)
+      primal_impl<double>(c, 1, k, kv, dl, dd, st);
+    else
+      primal_impl<float>(c, 1, k, kv, dl, dd, st);
+    d2h(c, dz_out, dd, es * P, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int b2p_reconstruct_primal_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd,
+                                          const void* lambda_dev, void* dz_dev, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(kd);
+    check_ctx(c);
+    if (batch < 1) throw invalid("reconstruct_primal: batch must be >= 1");
+    if (!lambda_dev || !dz_dev) throw invalid("reconstruct_primal: null buffer");
+    const KktDev kv = dev_view(kd);
+    if (dtype == B2P_F64)
+      primal_impl<double>(c, batch, kd, kv, lambda_dev, dz_dev, c->stream());
+    else
+      primal_impl<float>(c, batch, kd, kv, lambda_dev, dz_dev, c->stream());
+  });
+}
+
 int b2p_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd, int kind,
                              int order, const b2p_pcg_config* cfg, const void* lambda0_dev,
                              void* lambda_out_dev, b2p_solve_report* reports, int32_t* status_dev,

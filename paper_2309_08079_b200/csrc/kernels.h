@@ -104,6 +104,16 @@ template <class T> int fg_pick_rp(int K, int n, int m, int kind, int sm_count, i
 template <class T>
 cudaError_t launch_fg(const FusedParams<T>& p, const FgSync<T>& sy, int rp, cudaStream_t st);
 
+// reconstruct_primal (primal_kernels.cu): one warp per (system, knot, block).
+template <class T>
+struct PrimalParams {
+  int B, N, n, m;
+  const T *Q, *q, *R, *r, *A, *B_;  // b2p_kkt layout, [B][...]
+  const T* lambda;                 // [B][(N+1) n]
+  T* dz;                           // [B][(N+1) n + N m]
+};
+template <class T> cudaError_t launch_reconstruct_primal(const PrimalParams<T>& p, cudaStream_t st);
+
 // Shared-memory footprint of one PCG CTA (bytes) for a parameter block.
 template <class T>
 size_t pcg_smem_bytes(const PcgParams<T>& p);

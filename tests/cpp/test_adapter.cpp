@@ -100,6 +100,29 @@ int main() {
     for (size_t i = 0; i < x.size(); ++i) w2 = std::fmax(w2, std::fabs(x[i] - a.lambda[i]));
     CHECK(w2 <= 1e-5);
   }
+  {  // reconstruct_primal: zero multipliers and identity G give dz = -g (test_kkt.cpp:101-109)
+    KKTSystem kkt = random_kkt_family(0, 31, 3, 2, 1);
+    for (auto& kd : kkt.knots) {
+      kd.Q = Matrix::identity(2);
+      if (!kd.R.a.empty()) kd.R = Matrix::identity(1);
+    }
+    const Vector dz = reconstruct_primal(kkt, Vector(kkt.dual_dim(), 0.0));
+    double worst = 0.0;
+    size_t off = 0;
+    for (int k = 0; k <= kkt.N; ++k) {
+      for (double v : kkt.knots[k].q) worst = std::fmax(worst, std::fabs(dz[off++] + v));
+      if (k < kkt.N)
+        for (double v : kkt.knots[k].r) worst = std::fmax(worst, std::fabs(dz[off++] + v));
+    }
+    CHECK(off == dz.size() && worst <= 1e-14);
+    bool thrown = false;
+    try {
+      reconstruct_primal(kkt, Vector(5, 0.0));
+    } catch (const std::invalid_argument& e) {
+      thrown = std::string(e.what()) == "reconstruct_primal: expected lambda of length 8, got 5";
+    }
+    CHECK(thrown);
+  }
   {  // boundary padding rejects mutation (test_block_tri.cpp:91-95)
     BlockTriMatrix M(3, 2);
     bool t1 = false, t2 = false;

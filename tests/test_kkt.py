@@ -1,0 +1,100 @@
+"""Port of the reconstruct_primal cases of proj/tests/test_kkt.cpp (SURVEY §8f
+rank 1: the "Trajopt PPCG finish", kkt.cpp:153-181). Every case runs on the
+oracle and, marked gpu, on the B200 kernel through the C-ABI."""
+import numpy as np
+import pytest
+
+from backends import B  # noqa: F401
+from paper_2309_08079_b200.types import KKTSystem
+from util import dense_C, dense_G, dense_g, dense_schur_matrix, dense_schur_rhs, standard_batch
+
+
+def kkt_residual(kkt, dz, lam):  # test_kkt.cpp:17-26
+    G, C, g, c = dense_G(kkt), dense_C(kkt), dense_g(kkt), kkt.constraint_rhs()
+    stationarity = np.abs(G @ dz + g + C.T @ lam).max()
+    primal = np.abs(C @ dz - c).max()
+    scale = max(1.0, np.abs(g).max(), np.abs(c).max())
+    return max(stationarity, primal) / scale
+
+
+def dense_kkt_solve(kkt):  # kkt.cpp:129-151
+    G, C = dense_G(kkt), dense_C(kkt)
+    npd, nd = G.shape[0], C.shape[0]
+    K = np.zeros((npd + nd, npd + nd))
+    K[:npd, :npd] = G
+    K[:npd, npd:] = C.T
+    K[npd:, :npd] = C
+    sol = np.linalg.solve(K, np.concatenate([-dense_g(kkt), kkt.constraint_rhs()]))
+    return sol[:npd], sol[npd:]
+
+
+def test_zero_multipliers_identity_G_give_minus_g(B, orc):  # test_kkt.cpp:101-109
+    kkt = orc.random_kkt(31, 3, 2, 1)
+    kkt.Q[:] = np.eye(2)
+    kkt.R[:] = np.eye(1)
+    dz = B.reconstruct_primal(kkt, np.zeros(kkt.dual_dim()))
+    assert np.abs(dz + dense_g(kkt)).max() <= 1e-14
+
+
+def test_matches_dense_oracle_primal(B, orc):  # :110-115
+    kkt = orc.random_kkt(32, 4, 3, 2)
+    dz_ref, lam = dense_kkt_solve(kkt)
+    dz = B.reconstruct_primal(kkt, lam)
+    assert np.abs(dz - dz_ref).max() <= 1e-8
+
+
+def test_degenerate_single_knot_horizon(B):  # :116-128
+    kkt = KKTSystem(0, 3, 0, Q=np.eye(3)[None].copy(), q=np.ones((1, 3)),
+                    R=np.zeros((0, 0, 0)), r=np.zeros((0, 0)), A=np.zeros((0, 3, 3)),
+                    B=np.zeros((0, 3, 0)), e=np.zeros((0, 3)), x_s=np.zeros(3), x0=np.zeros(3))
+    dz = B.reconstruct_primal(kkt, np.zeros(3))
+    assert np.abs(dz + np.ones(3)).max() == 0.0
+
+
+def test_exact_dual_solve_closes_both_kkt_rows(B, orc):  # :131-142
+    for seed, N, n, m in standard_batch(10):
+        kkt = orc.random_kkt(seed, N, n, m)
+        lam = np.linalg.solve(dense_schur_matrix(kkt), dense_schur_rhs(kkt))
+        dz = B.reconstruct_primal(kkt, lam)
+        assert kkt_residual(kkt, dz, lam) <= 1e-8
+        assert np.abs(dense_C(kkt) @ dz - kkt.constraint_rhs()).max() <= 1e-8
+
+
+def test_lambda_length_message(B, orc):  # kkt.cpp:154-158
+    kkt = orc.random_kkt(33, 3, 2, 1)
+    with pytest.raises(ValueError, match="reconstruct_primal: expected lambda of length 8, got 5"):
+        B.reconstruct_primal(kkt, np.zeros(5))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(63, 14, 7), (511, 28, 14), (255, 12, 4)])
+def test_b200_matches_oracle_at_baseline_shapes(orc, shape):
+    import paper_2309_08079_b200.api as api
+    api.require_device()
+    N, n, m = shape
+    kkt = orc.random_kkt(7 + N, N, n, m)
+    lam = orc.solve(kkt).lambda_
+    want = orc.reconstruct_primal(kkt, lam)
+    got = api.reconstruct_primal(kkt, lam)
+    scale = max(1.0, np.abs(want).max())
+    assert np.abs(got - want).max() / scale <= 1e-12
+
+
+@pytest.mark.gpu
+def test_b200_batched_device_matches_single(orc):
+    import torch
+    import paper_2309_08079_b200.api as api
+    api.require_device()
+    Bn, N, n, m = 6, 31, 14, 7
+    kb = api.random_kkt_batch(500, Bn, N, n, m)
+    lam = np.stack([orc.solve(kb.system(i)).lambda_ for i in range(Bn)])
+    dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in kb.arrays()]
+    kd = KKTSystem(N, n, m, *dev)
+    lam_d = torch.from_numpy(lam).cuda()
+    dz_d = torch.empty((Bn, kb.primal_dim()), dtype=torch.float64, device="cuda")
+    api.reconstruct_primal_batched_device(kd, lam_d.data_ptr(), dz_d.data_ptr(), Bn)
+    torch.cuda.synchronize()
+    got = dz_d.cpu().numpy()
+    for i in range(Bn):
+        want = orc.reconstruct_primal(kb.system(i), lam[i])
+        assert np.abs(got[i] - want).max() / max(1.0, np.abs(want).max()) <= 1e-12
