@@ -156,23 +156,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // copy (sQi) and are inverted in place; lanes read their rows from smem.
     if (tid == 0) tma_load_1d(sQi, Qs, static_cast<unsigned>(sizeof(T) * K * nn), mbar_addr);
     mbar_wait(mbar_addr, mbar_phase);
+    // Both half-warps of a warp always run the same code (out-of-range knots
+    // recompute a clamped duplicate and store nothing), so every shuffle and
+    // sync below uses the full-warp mask.
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
       const int k = h + r * kHalfWarps;
-      if (k < K) {
+      {
+        const bool kv = k < K;
+        const int kc = kv ? k : K - 1;
         T a[NB], x[NB];
-        const T* Qr = sQi + static_cast<size_t>(k) * nn + lr * NB;
+        const T* Qr = sQi + static_cast<size_t>(kc) * nn + lr * NB;
 #pragma unroll
         for (int i = 0; i < NB; i += 2) {
           const double2 q2 = *reinterpret_cast<const double2*>(Qr + i);
           a[i] = q2.x;
           a[i + 1] = q2.y;
         }
-        const int f = hw_spd_inverse_v2<T, NB>(a, tW, tX, rd, l, x);
-        __syncwarp(hw_mask());  // every lane has consumed its Q_k row: overwrite in place
+        const int f = hw_spd_inverse_v2<T, NB, true>(a, tW, tX, rd, l, x);
+        __syncwarp();  // every lane has consumed its Q_k row: overwrite in place
         // first failing call in row order: row k as its Q_{k+1} (key 4k+2), or row 0
-        if (f >= 0) fkey = min(fkey, k == 0 ? 0 : 4 * k + 2);
-        if (lact) {
+        if (kv && f >= 0) fkey = min(fkey, k == 0 ? 0 : 4 * k + 2);
+        if (kv && lact) {
           T qq = T(0);
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
@@ -182,15 +187,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           sqq[k * 16 + l] = qq;
         }
       }
-      if (k < N) {
+      {
+        const bool kv = k < N;
+        const int kc = kv ? k : N - 1;
         T a[MB], x[MB];
         const int lm = l < MB ? l : MB - 1;
-        const T* Rr = Rs + static_cast<size_t>(k) * mm + lm * MB;
+        const T* Rr = Rs + static_cast<size_t>(kc) * mm + lm * MB;
 #pragma unroll
         for (int i = 0; i < MB; ++i) a[i] = Rr[i];
-        const int f = hw_spd_inverse_v2<T, MB>(a, tW, tX, rd, l, x);
-        if (f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
-        if (l < MB) {
+        const int f = hw_spd_inverse_v2<T, MB, true>(a, tW, tX, rd, l, x);
+        if (kv && f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
+        if (kv && l < MB) {
           T rr = T(0);
 #pragma unroll
           for (int i = 0; i < MB; ++i) {
@@ -207,9 +214,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // ============================================================ F2: rows
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
-      const int b = h + r * kHalfWarps;
-      if (b >= K) continue;
-      if (b == 0) {
+      const int b0 = h + r * kHalfWarps;
+      // rows outside [1, K) run the general path on row 1 and store nothing
+      // (keeps the two half-warps convergent for the full-warp shuffles)
+      const bool wr = b0 >= 1 && b0 < K;
+      const int b = wr ? b0 : 1;
+      if (b0 == 0) {
         // schur.cpp:53-57: S(0,0) = Q0^-1, theta_inv[0] = sym(Q0), gamma_0
         if (lact) {
 #pragma unroll
@@ -219,7 +229,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           }
           gG[l] = -((xs[l] - x0[l]) + sqq[l]);
         }
-        continue;
       }
       const int k = b - 1;
       const T* Ak = As + k * nn;
@@ -242,12 +251,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           x[i] = s;
         }
       }
-      __syncwarp(hw_mask());
+      __syncwarp();
       if (lact) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           tW[i * LD + l] = x[i];
-          gL[static_cast<size_t>(b) * nn + i * NB + l] = -x[i];
+          if (wr) gL[static_cast<size_t>(b) * nn + i * NB + l] = -x[i];
         }
       }
       // BR = B_k R_k^-1, column l < m
@@ -264,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           if (l < MB) tBR[i * LDM + l] = s;
         }
       }
-      __syncwarp(hw_mask());
+      __syncwarp();
       // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
       T arow[NB], brow[MB];
 #pragma unroll
@@ -292,10 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int q = 0; q < MB; ++q) brr += brow[q] * srr[k * 8 + q];
         const T zeta = (-aqq - brr) + sqq[(k + 1) * 16 + lr];
-        if (lact) gG[static_cast<size_t>(b) * NB + l] = -(-__ldg(es + k * NB + l) + zeta);
+        if (wr && lact) gG[static_cast<size_t>(b) * NB + l] = -(-__ldg(es + k * NB + l) + zeta);
       }
-      hw_symmetrize_col<T, NB, LD>(tW, l, x);  // theta (schur.cpp:67)
-      if (lact) {
+      hw_symmetrize_col<T, NB, LD, true>(tW, l, x);  // theta (schur.cpp:67)
+      if (wr && lact) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) gD[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
       }
@@ -304,10 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         T th[NB];
 #pragma unroll
         for (int i = 0; i < NB; ++i) th[i] = x[i];
-        const int f = hw_spd_inverse_v2<T, NB>(th, tW, tX, rd, l, x);
-        if (f >= 0) fkey = min(fkey, b * 4 + 3);
+        const int f = hw_spd_inverse_v2<T, NB, true>(th, tW, tX, rd, l, x);
+        if (wr && f >= 0) fkey = min(fkey, b * 4 + 3);
       }
-      if (lact) {
+      if (wr && lact) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) gT[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
       }

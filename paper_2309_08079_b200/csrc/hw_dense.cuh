@@ -85,18 +85,21 @@ __device__ __forceinline__ void hw_inv_col(const T* L, const T* rd, int j, T (&x
 }
 
 // column j of X -> column j of 0.5 (X + X') through the tile W (overwritten).
-template <class T, int N, int LD>
+// FW: both half-warps of the warp call together (convergent) -> full-warp
+// masks, no divergence bookkeeping around the shuffles / syncs.
+template <class T, int N, int LD, bool FW = false>
 __device__ __forceinline__ void hw_symmetrize_col(T* W, int j, T (&x)[N]) {
-  __syncwarp(hw_mask());
+  const unsigned mk = FW ? FULL : hw_mask();
+  __syncwarp(mk);
   if (j < N) {
 #pragma unroll
     for (int i = 0; i < N; ++i) W[i * LD + j] = x[i];
   }
-  __syncwarp(hw_mask());
+  __syncwarp(mk);
   const int jr = j < N ? j : N - 1;
 #pragma unroll
   for (int i = 0; i < N; ++i) x[i] = T(0.5) * (x[i] + W[jr * LD + i]);
-  __syncwarp(hw_mask());
+  __syncwarp(mk);
 }
 
 // W <- G (row-major N x N global), cooperative over the half-warp.
@@ -214,17 +217,17 @@ namespace hwd {
 //    X[i][l] and X[l][i]; the extra terms are exact zeros), so the
 //    0.5 (X + X') of the reference is the identity on it.
 // Out: x[] = row l (= column l) of W^-1. Returns the failing pivot or -1.
-template <class T, int N>
+template <class T, int N, bool FW = false>
 __device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd, int l,
                                                  T (&x)[N]) {
-  static_assert(N % 2 == 0 || sizeof(T) == 4 || true, "");
+  const unsigned mk = FW ? FULL : hw_mask();
   int fail = -1;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     T s = a[k];
 #pragma unroll
     for (int q = 0; q < k; ++q) s -= a[q] * Lr[k * N + q];
-    T piv = __shfl_sync(hw_mask(), s, k, 16);
+    T piv = __shfl_sync(mk, s, k, 16);
     if (piv <= T(0)) {
       if (fail < 0) fail = k;
       piv = T(1);
@@ -238,7 +241,7 @@ __device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd
       a[k] = s * r;
       Lr[l * N + k] = a[k];
     }
-    __syncwarp(hw_mask());
+    __syncwarp(mk);
   }
   // column l of L^-1 (zero above the diagonal)
   T y[N];
@@ -253,7 +256,7 @@ __device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd
 #pragma unroll
     for (int q = 0; q < N; ++q) LiT[l * N + q] = y[q];
   }
-  __syncwarp(hw_mask());
+  __syncwarp(mk);
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     T s = T(0);
@@ -261,7 +264,7 @@ __device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd
     for (int q = i; q < N; ++q) s += LiT[i * N + q] * y[q];
     x[i] = s;
   }
-  __syncwarp(hw_mask());
+  __syncwarp(mk);
   return fail;
 }
 
