@@ -234,22 +234,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       const T* Ak = As + k * nn;
       const T* Bk = Bs + k * nm;
       T x[NB];
-      // AQ = A_k Q_k^-1, column l  ->  L_b = phi = -AQ   (schur.cpp:68)
+      // A_k -> the tX tile with asynchronous 16-byte copies (one L2 round trip,
+      // no registers held), then AQ = A_k Q_k^-1 column l from shared memory
+      // -> L_b = phi = -AQ (schur.cpp:68)
       {
-        T qc[NB];
+        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(tX));
+        for (int c = l; c < NN / 2; c += 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16u * c),
+                       "l"(Ak + 2 * c)
+                       : "memory");
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+      }
+      T qc[NB];
 #pragma unroll
-        for (int q = 0; q < NB; ++q) qc[q] = sQi[k * NN + q * NB + lr];
+      for (int q = 0; q < NB; ++q) qc[q] = sQi[k * NN + q * NB + lr];
+      __syncwarp();
+      {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           T s = T(0);
 #pragma unroll
           for (int q = 0; q < NB; q += 2) {
-            const double2 a2 = __ldg(reinterpret_cast<const double2*>(Ak + i * NB + q));
+            const double2 a2 = *reinterpret_cast<const double2*>(tX + i * NB + q);
             s += a2.x * qc[q];
             s += a2.y * qc[q + 1];
           }
           x[i] = s;
         }
+      }
+      T arow[NB];
+#pragma unroll
+      for (int q = 0; q < NB; q += 2) {
+        const double2 a2 = *reinterpret_cast<const double2*>(tX + lr * NB + q);
+        arow[q] = a2.x;
+        arow[q + 1] = a2.y;
       }
       __syncwarp();
       if (lact) {
@@ -275,13 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       }
       __syncwarp();
       // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
-      T arow[NB], brow[MB];
-#pragma unroll
-      for (int q = 0; q < NB; q += 2) {
-        const double2 a2 = __ldg(reinterpret_cast<const double2*>(Ak + lr * NB + q));
-        arow[q] = a2.x;
-        arow[q + 1] = a2.y;
-      }
+      T brow[MB];
 #pragma unroll
       for (int q = 0; q < MB; ++q) brow[q] = __ldg(Bk + lr * MB + q);
 #pragma unroll
