@@ -237,13 +237,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       // A_k -> the tX tile with asynchronous 16-byte copies (one L2 round trip,
       // no registers held), then AQ = A_k Q_k^-1 column l from shared memory
       // -> L_b = phi = -AQ (schur.cpp:68)
+      // R_k^-1 (from the slot, 8-byte aligned) -> the tW tile the same way
+      T brow[MB];
+#pragma unroll
+      for (int q = 0; q < MB; ++q) brow[q] = __ldg(Bk + lr * MB + q);
       {
         const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(tX));
         for (int c = l; c < NN / 2; c += 16)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16u * c),
                        "l"(Ak + 2 * c)
                        : "memory");
+        const unsigned dr = static_cast<unsigned>(__cvta_generic_to_shared(tW));
+        for (int c = l; c < MB * MB; c += 16)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dr + 8u * c),
+                       "l"(gR + static_cast<size_t>(k) * mm + c)
+                       : "memory");
         asm volatile("cp.async.wait_all;\n" ::: "memory");
+      }
+      __syncwarp();
+      // BR = B_k R_k^-1, row l (R_k^-1 rows are broadcasts)
+      T br[MB];
+#pragma unroll
+      for (int q = 0; q < MB; ++q) br[q] = T(0);
+#pragma unroll
+      for (int s2 = 0; s2 < MB; ++s2) {
+#pragma unroll
+        for (int q = 0; q < MB; ++q) br[q] += brow[s2] * tW[s2 * MB + q];
       }
       T qc[NB];
 #pragma unroll
@@ -269,33 +288,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         arow[q] = a2.x;
         arow[q + 1] = a2.y;
       }
-      __syncwarp();
+      __syncwarp();  // A_k and R_k^-1 tiles consumed
       if (lact) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           tW[i * LD + l] = x[i];
           if (wr) gL[static_cast<size_t>(b) * nn + i * NB + l] = -x[i];
         }
-      }
-      // BR = B_k R_k^-1, column l < m
-      {
-        const int lm = l < MB ? l : MB - 1;
-        T rc[MB];
 #pragma unroll
-        for (int q = 0; q < MB; ++q) rc[q] = __ldcg(gR + static_cast<size_t>(k) * mm + q * MB + lm);
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          T s = T(0);
-#pragma unroll
-          for (int q = 0; q < MB; ++q) s += __ldg(Bk + i * MB + q) * rc[q];
-          if (l < MB) tBR[i * LDM + l] = s;
-        }
+        for (int q = 0; q < MB; ++q) tBR[l * LDM + q] = br[q];
       }
       __syncwarp();
       // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
-      T brow[MB];
-#pragma unroll
-      for (int q = 0; q < MB; ++q) brow[q] = __ldg(Bk + lr * MB + q);
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
         T s1 = T(0), s2 = T(0);
