@@ -46,7 +46,8 @@ struct FLayout {
   __host__ __device__ static int oqq(int K) { return K * NB * NB; }
   __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
   __host__ __device__ static int ohw(int K) { return orr(K) + (K - 1) * 8; }
-  __host__ __device__ static int total(int K) { return ohw(K) + kHalfWarps * per_hw; }
+  __host__ __device__ static int osq(int K) { return ohw(K) + kHalfWarps * per_hw; }  // q_k
+  __host__ __device__ static int total(int K) { return osq(K) + K * NB; }
 };
 
 }  // namespace
@@ -65,6 +66,16 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uns
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
                "r"(bytes)
                : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst_smem))),
+      "l"(src), "r"(bytes), "r"(mbar_addr)
+      : "memory");
+}
+// Second bulk copy completing on the same mbarrier phase (the first call's
+// expect_tx must have covered its bytes).
+__device__ __forceinline__ void tma_copy_1d(void* dst_smem, const void* src, unsigned bytes,
+                                            unsigned mbar_addr) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
       "[%3];\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst_smem))),
@@ -154,7 +165,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // by the two block rows that use them (the reference recomputes them per
     // row, schur.cpp:49-51; same arithmetic). All Q_k arrive in one TMA bulk
     // copy (sQi) and are inverted in place; lanes read their rows from smem.
-    if (tid == 0) tma_load_1d(sQi, Qs, static_cast<unsigned>(sizeof(T) * K * nn), mbar_addr);
+    T* sq = smem + FL::osq(K);  // q_k of every knot (for Q_k^-1 q_k)
+    if (tid == 0) {
+      const unsigned bq = static_cast<unsigned>(sizeof(T) * K * nn);
+      const unsigned bv = static_cast<unsigned>(sizeof(T) * K * NB);
+      asm volatile("fence.proxy.async;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
+                   "r"(bq + bv)
+                   : "memory");
+      tma_copy_1d(sQi, Qs, bq, mbar_addr);
+      tma_copy_1d(sq, qs, bv, mbar_addr);
+    }
     mbar_wait(mbar_addr, mbar_phase);
     // Both half-warps of a warp always run the same code (out-of-range knots
     // recompute a clamped duplicate and store nothing), so every shuffle and
@@ -162,6 +183,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll 1
     for (int r = 0; r < R; ++r) {
       const int k = h + r * kHalfWarps;
+      // R_k row l issued before the Q_k inverse so its L2 latency is hidden
+      T ra[MB];
+      {
+        const int kc = k < N ? k : N - 1;
+        const int lm = l < MB ? l : MB - 1;
+        const T* Rr = Rs + static_cast<size_t>(kc) * mm + lm * MB;
+#pragma unroll
+        for (int i = 0; i < MB; ++i) ra[i] = __ldg(Rr + i);
+      }
       {
         const bool kv = k < K;
         const int kc = kv ? k : K - 1;
@@ -182,20 +212,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
           for (int i = 0; i < NB; ++i) {
             sQi[k * NN + i * NB + l] = x[i];
-            qq += x[i] * qs[k * NB + i];
+            qq += x[i] * sq[k * NB + i];
           }
           sqq[k * 16 + l] = qq;
         }
       }
       {
         const bool kv = k < N;
-        const int kc = kv ? k : N - 1;
-        T a[MB], x[MB];
-        const int lm = l < MB ? l : MB - 1;
-        const T* Rr = Rs + static_cast<size_t>(kc) * mm + lm * MB;
-#pragma unroll
-        for (int i = 0; i < MB; ++i) a[i] = Rr[i];
-        const int f = hw_spd_inverse_v2<T, MB, true>(a, tW, tX, rd, l, x);
+        T x[MB];
+        const int f = hw_spd_inverse_v2<T, MB, true>(ra, tW, tX, rd, l, x);
         if (kv && f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
         if (kv && l < MB) {
           T rr = T(0);
