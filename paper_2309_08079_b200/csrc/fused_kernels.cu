@@ -95,8 +95,73 @@ __device__ __forceinline__ void mbar_wait(unsigned mbar_addr, unsigned& phase) {
   phase ^= 1u;
 }
 
+// ---- Tensor memory (TMEM) as a third on-chip operand store for the PCG
+// phase: 512 columns x 128 lanes x 32 bit; thread t of warp w owns TMEM lane
+// 32*(w%4) + t%32 and columns [128*(w/4), 128*(w/4) + 128): D_b row l and L_b
+// row l of its R = 2 block rows, 32 columns (14 doubles + pad) each.
+// Measured tcgen05.ld throughput ~390 B/clk/SM vs 128 B/clk for shared memory
+// (scripts/micro/tmem_bench.cu), so the row products come from TMEM and only
+// the column products R_b = L_{b+1}' read shared memory.
+__device__ __forceinline__ void tm_st_row14(unsigned taddr, const double (&v)[14]) {
+  unsigned u[28];
+#pragma unroll
+  for (int j = 0; j < 14; ++j) {
+    u[2 * j] = static_cast<unsigned>(__double2loint(v[j]));
+    u[2 * j + 1] = static_cast<unsigned>(__double2hiint(v[j]));
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16};\n" ::"r"(taddr),
+      "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]),
+      "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15])
+      : "memory");
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr + 16),
+      "r"(u[16]), "r"(u[17]), "r"(u[18]), "r"(u[19]), "r"(u[20]), "r"(u[21]), "r"(u[22]), "r"(u[23])
+      : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr + 24),
+               "r"(u[24]), "r"(u[25]), "r"(u[26]), "r"(u[27])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld_row14(unsigned taddr, double (&v)[14]) {
+  unsigned u[28];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+        "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+        "=r"(u[14]), "=r"(u[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
+                 "=r"(u[22]), "=r"(u[23])
+               : "r"(taddr + 16)
+               : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27])
+               : "r"(taddr + 24)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 14; ++j) v[j] = __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j]));
+}
+// sum_j m[j] x[j] (m in registers, x a 16-byte aligned shared vector), two partial sums
+template <int NB>
+__device__ __forceinline__ double dot_rm(const double (&m)[NB], const double* x) {
+  double a = 0.0, c = 0.0;
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(x + j);
+    a += m[j] * v.x;
+    c += m[j + 1] * v.y;
+  }
+  return a + c;
+}
+
 template <class T, int NB, int MB, int R>
 __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
+  static_assert(NB == 14 && sizeof(T) == 8, "TMEM row layout is written for n = 14, fp64");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using FL = FLayout<T, NB, MB>;
   constexpr int NN = NB * NB;
@@ -109,9 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   const bool lact = l < NB;
   T* smem = reinterpret_cast<T*>(smem_raw);
   // PCG layout
-  T* sL = smem;                          // [K][NB][NB]
-  T* sD = sL + static_cast<size_t>(K) * NN;  // [K][NB][NB]
-  T* sp = sD + static_cast<size_t>(K) * NN;  // [K][NB]
+  T* sL = smem;                          // [K][NB][NB] (column products)
+  T* sp = sL + static_cast<size_t>(K) * NN;  // [K][NB]
   T* st = sp + K * NB;
   T* su = st + K * NB;
   T* red = su + K * NB;                  // [64]
@@ -123,11 +187,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   __shared__ __align__(8) unsigned long long s_mbar;  // TMA staging barrier
   const unsigned mbar_addr = static_cast<unsigned>(__cvta_generic_to_shared(&s_mbar));
   unsigned mbar_phase = 0;
+  __shared__ unsigned s_taddr;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar_addr) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if ((tid >> 5) == 0) {  // warp 0 owns the whole TMEM of the SM (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(&s_taddr)))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const unsigned tbase = s_taddr + ((32u * ((tid >> 5) & 3)) << 16) + 128u * (tid >> 7);
+  auto colD = [&](int r) { return tbase + 32u * r; };
+  auto colL = [&](int r) { return tbase + 64u + 32u * r; };
   // CTA-private global slot (L2 resident)
   T* gL = p.slot + static_cast<size_t>(blockIdx.x) * (3 * K * NN + K * NB + K * MB * MB);
   T* gD = gL + static_cast<size_t>(K) * NN;
@@ -248,10 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         // schur.cpp:53-57: S(0,0) = Q0^-1, theta_inv[0] = sym(Q0), gamma_0
         if (lact) {
 #pragma unroll
-          for (int i = 0; i < NB; ++i) {
-            gD[i * NB + l] = sQi[i * NB + l];
-            gT[i * NB + l] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
-          }
+          for (int i = 0; i < NB; ++i) gT[i * NB + l] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
           gG[l] = -((xs[l] - x0[l]) + sqq[l]);
         }
       }
@@ -324,6 +397,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int q = 0; q < MB; ++q) tBR[l * LDM + q] = br[q];
       }
       __syncwarp();
+      {  // row l of L_b = -AQ -> TMEM (the row products of the PCG phase)
+        T lrow[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) lrow[j] = -tW[lr * LD + j];
+        tm_st_row14(colL(r), lrow);
+      }
       // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
@@ -345,9 +424,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         if (wr && lact) gG[static_cast<size_t>(b) * NB + l] = -(-__ldg(es + k * NB + l) + zeta);
       }
       hw_symmetrize_col<T, NB, LD, true>(tW, l, x);  // theta (schur.cpp:67)
-      if (wr && lact) {
+      {  // row l of D_b = theta (row 0: Q_0^-1, schur.cpp:53) -> TMEM
+        T drow[NB];
 #pragma unroll
-        for (int i = 0; i < NB; ++i) gD[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
+        for (int i = 0; i < NB; ++i) drow[i] = (b0 == 0) ? sQi[lr * NB + i] : x[i];
+        tm_st_row14(colD(r), drow);
       }
       // theta^-1 (schur.cpp:75): x holds row l of the symmetric theta
       {
@@ -362,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int i = 0; i < NB; ++i) gT[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
       }
     }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     if (tm) tm[2] = gtimer();
     if (l == 0 && fkey != 0x7fffffff) atomicMin(&s_err, fkey);
     __syncthreads();
@@ -383,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // bulk copy completed on an mbarrier; then prefetch the next system's
     // KKT inputs into L2 so its formation phase does not start on cold HBM.
     {
-      const unsigned bytes = static_cast<unsigned>(sizeof(T) * 2 * K * NN);
+      const unsigned bytes = static_cast<unsigned>(sizeof(T) * K * NN);
       if (tid == 0) tma_load_1d(sL, gL, bytes, mbar_addr);
       const int nsys = sys + gridDim.x;
       if (nsys < p.B && tid < 9) {
@@ -434,17 +516,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       const T *Mp[R], *Xp[R];
       T sd[R], sl[R], sr[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        Mp[r] = sD + static_cast<size_t>(bc[r]) * NN + l * NB;
-        Xp[r] = x + bc[r] * NB;
+      for (int r = 0; r < R; ++r) {  // D_b and L_b rows from TMEM
+        T m[NB];
+        tm_ld_row14(colD(r), m);
+        sd[r] = dot_rm<NB>(m, x + bc[r] * NB);
+        tm_ld_row14(colL(r), m);
+        sl[r] = dot_rm<NB>(m, x + (bc[r] - 1) * NB);
       }
-      dots_row<T, NB, R>(Mp, Xp, sd);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        Mp[r] = sL + static_cast<size_t>(bc[r]) * NN + l * NB;
-        Xp[r] = x + (bc[r] - 1) * NB;
-      }
-      dots_row<T, NB, R>(Mp, Xp, sl);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         Mp[r] = sL + static_cast<size_t>(bc[r] + 1) * NN + l;
@@ -498,10 +576,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         const T *Mp[R], *Xp[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          Mp[r] = sL + static_cast<size_t>(bc[r]) * NN + l * NB;
-          Xp[r] = st + (bc[r] - 1) * NB;
+          T m[NB];
+          tm_ld_row14(colL(r), m);
+          sl[r] = dot_rm<NB>(m, st + (bc[r] - 1) * NB);
         }
-        dots_row<T, NB, R>(Mp, Xp, sl);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           Mp[r] = sL + static_cast<size_t>(bc[r] + 1) * NN + l;
@@ -635,12 +713,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       if (tm) tm[4] = gtimer();
     }
   }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if ((tid >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(s_taddr) : "memory");
 }
 
 template <class T, int NB, int MB>
 size_t fused_smem_bytes(int K) {
   using FL = FLayout<T, NB, MB>;
-  const size_t pcg = sizeof(T) * (static_cast<size_t>(2) * K * NB * NB + 3 * K * NB + 64);
+  const size_t pcg = sizeof(T) * (static_cast<size_t>(K) * NB * NB + 3 * K * NB + 64);
   const size_t form = sizeof(T) * static_cast<size_t>(FL::total(K));
   return std::max(pcg, form);
 }
