@@ -132,10 +132,18 @@ __device__ __forceinline__ T block_reduce(T v, T* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) red[warp] = v;
   __syncthreads();
-  T s = T(0);
+  // pairwise tree over the warp partials (fixed order: every thread gets the
+  // bit-identical sum; depth log2(#warps) instead of a #warps-long DADD chain)
+  constexpr int NW = kThreads / 32;
+  T t[NW];
 #pragma unroll
-  for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-  return s;
+  for (int w = 0; w < NW; ++w) t[w] = red[w];
+#pragma unroll
+  for (int st = 1; st < NW; st <<= 1) {
+#pragma unroll
+    for (int w = 0; w + st < NW; w += 2 * st) t[w] += t[w + st];
+  }
+  return t[0];
 }
 
 // ---------------------------------------------------------------- PCG row products
