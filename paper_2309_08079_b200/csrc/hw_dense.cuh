@@ -43,19 +43,14 @@ __device__ __forceinline__ int hw_cholesky(T* A, T* rd, int l) {
 #pragma unroll
     for (int p = 0; p < k; ++p) s -= A[lr * LD + p] * A[k * LD + p];
     T x = __shfl_sync(hw_mask(), s, k, 16);
-    if (x <= T(0)) {
-      if (fail < 0) fail = k;
-      x = T(1);
-    }
+    const bool bad = x <= T(0);  // branch-free: fails on x <= 0, NaN passes
+    fail = (bad && fail < 0) ? k : fail;
+    x = bad ? T(1) : x;
     const T r = rsqrt(x);  // one MUFU sequence per pivot: 1/L(k,k) and L(k,k) = x * r
-    const T d = x * r;
+    const T val = (l == k ? x : s) * r;
     __syncwarp(hw_mask());
-    if (l == k) {
-      A[k * LD + k] = d;
-      rd[k] = r;
-    } else if (l > k && l < N) {
-      A[l * LD + k] = s * r;
-    }
+    if (l >= k && l < N) A[l * LD + k] = val;
+    if (l == k) rd[k] = r;
     __syncwarp(hw_mask());
   }
   return fail;

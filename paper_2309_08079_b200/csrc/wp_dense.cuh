@@ -38,19 +38,16 @@ __device__ __forceinline__ int wp_spd_inverse(T (&a)[N], T* Lr, T* LiT, T* rd, i
 #pragma unroll
     for (int q = 0; q < k; ++q) s -= a[q] * Lr[k * N + q];
     T piv = __shfl_sync(FULL, s, k);
-    if (piv <= T(0)) {
-      if (fail < 0) fail = k;
-      piv = T(1);
-    }
+    // branch-free pivot step: x <= 0 fails (replaced by 1), NaN passes (Eigen LLT)
+    const bool bad = piv <= T(0);
+    fail = (bad && fail < 0) ? k : fail;
+    piv = bad ? T(1) : piv;
     const T r = rsqrt(piv);
-    if (l == k) {
-      a[k] = piv * r;
-      rd[k] = r;
-      Lr[k * N + k] = a[k];
-    } else if (l > k && l < N) {
-      a[k] = s * r;
-      Lr[l * N + k] = a[k];
-    }
+    const T val = (l == k ? piv : s) * r;
+    const bool own = l >= k && l < N;
+    a[k] = own ? val : a[k];
+    if (own) Lr[l * N + k] = val;
+    if (l == k) rd[k] = r;
     __syncwarp();
   }
   T y[N];
