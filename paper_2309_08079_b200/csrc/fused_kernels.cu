@@ -124,6 +124,10 @@ __device__ __forceinline__ void tm_st_row14(unsigned taddr, const double (&v)[14
                : "memory");
 }
 __device__ __forceinline__ void tm_ld_row14(unsigned taddr, double (&v)[14]) {
+  // No "memory" clobbers: the loads only write registers, so the compiler may
+  // keep scheduling shared-memory loads around them; the wait takes every
+  // destination register as an in/out operand, which keeps all consumers
+  // after it.
   unsigned u[28];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -131,18 +135,20 @@ __device__ __forceinline__ void tm_ld_row14(unsigned taddr, double (&v)[14]) {
       : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
         "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
         "=r"(u[14]), "=r"(u[15])
-      : "r"(taddr)
-      : "memory");
+      : "r"(taddr));
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
                : "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
                  "=r"(u[22]), "=r"(u[23])
-               : "r"(taddr + 16)
-               : "memory");
+               : "r"(taddr + 16));
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
                : "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27])
-               : "r"(taddr + 24)
-               : "memory");
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+               : "r"(taddr + 24));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]),
+                 "+r"(u[7]), "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]),
+                 "+r"(u[13]), "+r"(u[14]), "+r"(u[15]), "+r"(u[16]), "+r"(u[17]), "+r"(u[18]),
+                 "+r"(u[19]), "+r"(u[20]), "+r"(u[21]), "+r"(u[22]), "+r"(u[23]), "+r"(u[24]),
+                 "+r"(u[25]), "+r"(u[26]), "+r"(u[27]));
 #pragma unroll
   for (int j = 0; j < 14; ++j) v[j] = __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j]));
 }
