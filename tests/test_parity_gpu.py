@@ -247,3 +247,62 @@ def test_cluster_kernel_warm_start_and_errors(api, orc, env):
     bad.R[40] = -np.eye(7)
     with pytest.raises(RuntimeError, match="build_schur: R at knot 40 is not positive definite"):
         api.solve(bad)
+
+
+@pytest.mark.parametrize("kind", [PrecondKind.identity, PrecondKind.block_jacobi,
+                                  PrecondKind.stair, PrecondKind.symmetric_stair])
+@pytest.mark.parametrize("K", [32, 64, 40])
+def test_one_cta_fused_kernel_every_preconditioner(api, orc, env, kind, K):
+    """The c4 one-CTA kernel (TMEM operand store) for every preconditioner kind,
+    full (R = 1, 2) and ragged (K = 40: clamped duplicate half-warps) horizons."""
+    env["B2P_FC"] = "0"
+    B = 12  # > 8: batched path -> one-CTA fused kernel
+    kb = api.random_kkt_batch(7000 + K, B, K - 1, 14, 7)
+    cfg = PcgConfig(epsilon=1e-8)
+    lam, reps = api.solve_batched(kb, kind, cfg=cfg)
+    assert api.context().last_path() == 1
+    from paper_2309_08079_b200.types import PcgVariant
+    for i in (0, 5, 11):
+        want = orc.solve(kb.system(i), kind, cfg=cfg)
+        if want.report.iterations <= 20:  # the stair family: exact parity
+            assert reps[i].iterations == want.report.iterations
+        else:
+            # identity / Jacobi on kappa ~ 1e4: ~25-95 CG steps; the reference's own
+            # two variants (sequential vs block-parallel tree reductions,
+            # pcg.cpp:55-129 / :157-362) can already differ by one iteration here
+            par = orc.solve(kb.system(i), kind, cfg=PcgConfig(
+                epsilon=1e-8, variant=PcgVariant.block_parallel, deterministic_reductions=True))
+            assert reps[i].iterations in (want.report.iterations, par.report.iterations)
+        if want.report.iterations <= 20:
+            assert rel_inf_error(lam[i], want.lambda_) <= TOL64
+        else:
+            # identity / Jacobi: ~25-95 CG steps on kappa ~ 1e4 amplify rounding-order
+            # differences in lambda itself; both solves must reach the same true
+            # residual level (the reference's exit test is on r'r~, pcg.cpp:116)
+            sch = orc.build_schur(kb.system(i))
+            res = lambda x: float(np.linalg.norm(sch.gamma - sch.S.to_dense() @ x))
+            assert res(lam[i]) <= 10.0 * max(res(want.lambda_), np.sqrt(cfg.epsilon))
+
+
+def test_one_cta_fused_kernel_warm_start_cap_and_errors(api, orc, env):
+    env["B2P_FC"] = "0"
+    B, K = 10, 64
+    kb = api.random_kkt_batch(7100, B, K - 1, 14, 7)
+    cfg = PcgConfig(epsilon=1e-8)
+    want = [orc.solve(kb.system(i), PrecondKind.symmetric_stair, cfg=cfg) for i in range(B)]
+    l0 = np.stack([0.5 * w.lambda_ for w in want])
+    lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, cfg=cfg, lambda0=l0)
+    assert api.context().last_path() == 1
+    for i in (0, 9):
+        ow = orc.solve(kb.system(i), PrecondKind.symmetric_stair, cfg=cfg, lambda0=l0[i])
+        assert reps[i].iterations == ow.report.iterations
+        assert rel_inf_error(lam[i], ow.lambda_) <= TOL64
+    capped = PcgConfig(epsilon=1e-14, max_iter=3)
+    lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, cfg=capped)
+    oc = orc.solve(kb.system(3), PrecondKind.symmetric_stair, cfg=capped)
+    assert not reps[3].converged and reps[3].iterations == 3
+    assert rel_inf_error(lam[3], oc.lambda_) <= TOL64  # best iterate
+    bad = api.random_kkt_batch(7200, B, K - 1, 14, 7)
+    bad.Q[4][33] = -np.eye(14)  # knot 33: second half-warp pass (r = 1)
+    with pytest.raises(RuntimeError, match="build_schur: Q at knot 33 is not positive definite"):
+        api.solve_batched(bad, PrecondKind.symmetric_stair, cfg=cfg)
