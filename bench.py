@@ -93,6 +93,9 @@ def algorithmic(N, n, m, iters, w=8):
                 f_iter=f_iter, f_full=f_form + (iters + 1) * f_iter)
 
 
+FP64_PEAK_TFLOPS = 35.4  # measured on this pool's B200 (scripts/micro/lat_bench.cu)
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -381,7 +384,17 @@ def run_b200(a, world, rank, local):
                      "phase_ms_per_step": ({"K13_fused": k1_avg + k3_avg} if fused else
                                            {"K1_schur_formation": k1_avg, "K3_pcg": k3_avg}),
                      "fp64_tflops_step": flops_step / (elapsed_ms / a.steps * 1e-3) / 1e12,
-                     "b_full_GBs": B * alg["b_full"] / (elapsed_ms / a.steps * 1e-3) / 1e9},
+                     "b_full_GBs": B * alg["b_full"] / (elapsed_ms / a.steps * 1e-3) / 1e9,
+                     # the on-chip roof that actually binds this kernel: FP64 FMA work of
+                     # the reference algorithm (SURVEY 8d F_full) against the measured
+                     # DFMA peak (scripts/micro/lat_bench.cu: 60.9 FMA/clk/SM, 35.4 TF/s)
+                     "fp64": {"achieved": flops_step / (elapsed_ms / a.steps * 1e-3) / 1e12,
+                              "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": flops_step / (elapsed_ms / a.steps * 1e-3) / 1e12
+                              / FP64_PEAK_TFLOPS,
+                              "flops_per_step": flops_step,
+                              "peak_source": "measured DFMA microbenchmark "
+                                             "(scripts/micro/lat_bench.cu)"}},
         "pcg_iters": {"mean": mean_iters, "min": int(min(iters)), "max": int(max(iters))},
         "latency": latency,
         "clocks": clk.summary(),
