@@ -9,7 +9,8 @@ import paper_2309_08079_b200.api as api
 from paper_2309_08079_b200._lib import load
 from paper_2309_08079_b200.types import PcgConfig, PrecondKind
 B = int(os.environ.get("PB", "1184"))
-kb = api.random_kkt_batch(2309, B, 63, 14, 7)
+KN = int(os.environ.get("PK", "64"))
+kb = api.random_kkt_batch(2309, B, KN - 1, 14, 7)
 for _ in range(3):
     lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
 ctx = api.context()
