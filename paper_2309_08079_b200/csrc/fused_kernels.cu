@@ -165,6 +165,15 @@ __device__ __forceinline__ double dot_rm(const double (&m)[NB], const double* x)
   return a + c;
 }
 
+// per-CTA slot stride in elements, padded to 16 bytes (the TMA source must be aligned)
+template <class T>
+__host__ __device__ inline size_t fused_slot_stride(int K, int n, int m) {
+  const size_t e = static_cast<size_t>(2) * K * n * n + static_cast<size_t>(K) * n +
+                   static_cast<size_t>(K) * m * m;
+  const size_t a = 16 / sizeof(T);
+  return (e + a - 1) / a * a;
+}
+
 template <class T, int NB, int MB, int R>
 __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   static_assert(NB == 14 && sizeof(T) == 8, "TMEM row layout is written for n = 14, fp64");
@@ -211,9 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   auto colD = [&](int r) { return tbase + 32u * r; };
   auto colL = [&](int r) { return tbase + 64u + 32u * r; };
   // CTA-private global slot (L2 resident)
-  T* gL = p.slot + static_cast<size_t>(blockIdx.x) * (3 * K * NN + K * NB + K * MB * MB);
-  T* gD = gL + static_cast<size_t>(K) * NN;
-  T* gT = gD + static_cast<size_t>(K) * NN;
+  // CTA-private slot (L2 resident): L (TMA-staged for the column products),
+  // theta^-1, gamma, R^-1; D never leaves the SM (formation registers -> TMEM)
+  T* gL = p.slot + static_cast<size_t>(blockIdx.x) * fused_slot_stride<T>(K, NB, MB);
+  T* gT = gL + static_cast<size_t>(K) * NN;
   T* gG = gT + static_cast<size_t>(K) * NN;  // gamma [K][NB]
   T* gR = gG + static_cast<size_t>(K) * NB;  // R_k^-1 [N][MB][MB]
 
@@ -744,8 +754,7 @@ bool fused_supported(int K, int n, int m, int kind) {
 
 template <class T>
 size_t fused_slot_elems(int K, int n, int m) {
-  return static_cast<size_t>(3) * K * n * n + static_cast<size_t>(K) * n +
-         static_cast<size_t>(K) * m * m;
+  return fused_slot_stride<T>(K, n, m);
 }
 
 template <class T>

