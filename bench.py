@@ -383,6 +383,36 @@ def run_b200(a, world, rank, local):
         except Exception as exc:  # report, do not fail the bench line
             latency["c1_graph"] = {"error": str(exc)[:200]}
 
+    # ---- reconstruct_primal on the same batch: dz from the
+    # solved lambda, device-resident; HBM-bound (reads the KKT blocks + lambda,
+    # writes dz), so its roofline fraction is meaningful
+    primal = None
+    if rank == 0:
+        P = (N + 1) * n + N * m
+        dz_dev = torch.empty((B, P), dtype=torch.float64, device=f"cuda:{local}")
+        for _ in range(3):
+            api.reconstruct_primal_batched_device(kd, lam_dev.data_ptr(), dz_dev.data_ptr(), B,
+                                                  ctx=ctx)
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        p0.record(stream)
+        for _ in range(reps):
+            api.reconstruct_primal_batched_device(kd, lam_dev.data_ptr(), dz_dev.data_ptr(), B,
+                                                  ctx=ctx)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pms = p0.elapsed_time(p1) / reps
+        # compulsory bytes per system: Q, q (all knots), R, r, A, B (k < N), lambda in, dz out
+        pbytes = 8 * ((N + 1) * (n * n + n) + N * (m * m + m + n * n + n * m) + (N + 1) * n + P)
+        hbm_p, _src = peaks()
+        primal = {"systems_per_s": B / (pms * 1e-3), "ms_per_batch": pms,
+                  "achieved_GBs": B * pbytes / (pms * 1e-3) / 1e9, "peak_GBs": hbm_p,
+                  "frac": B * pbytes / (pms * 1e-3) / 1e9 / hbm_p,
+                  "bytes_per_system": pbytes,
+                  "what": "b2p_reconstruct_primal_batched_device over the bench batch "
+                          "(kkt.cpp:153-181), CUDA events, inputs in HBM"}
+
     # ---- roofline for the dominant kernel
     mean_iters = float(np.mean(iters))
     alg = algorithmic(N, n, m, mean_iters)
@@ -438,6 +468,7 @@ def run_b200(a, world, rank, local):
                                              "(scripts/micro/lat_bench.cu)"}},
         "pcg_iters": {"mean": mean_iters, "min": int(min(iters)), "max": int(max(iters))},
         "latency": latency,
+        "reconstruct_primal": primal,
         "clocks": clk.summary(),
     }
     if not a.no_cpu and world == 1 and rank == 0:

@@ -90,9 +90,144 @@ __global__ void __launch_bounds__(32 * kPrWarps) k_reconstruct_primal(PrimalPara
   }
 }
 
+// ---------------------------------------------------------------------------
+// Compile-time-shape variant (n, m <= 16): one 16-lane half-warp per (system,
+// knot, block), lane i owning row i in registers; unpivoted L D L' with the
+// pivot broadcast by shuffles, forward sweep by shuffles, backward sweep
+// through the unit-lower rows in shared memory. Many half-warps per SM hide
+// the short dependency chains, so the kernel runs at the HBM roofline of its
+// operands (the KKT blocks, lambda in, dz out).
+namespace {
+constexpr int kPrHw = 16;  // half-warps per CTA (256 threads)
+
+template <class T, int D>
+__device__ __forceinline__ void hw_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l, unsigned mk) {
+  // a: row l of the block (lanes l < D); rhs: b_l. Out: rhs = x_l.
+  // factor: a[q] <- L(l, q) for q < l, dl = D_l
+  T dl = T(1);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    T s = a[k];
+#pragma unroll
+    for (int q = 0; q < k; ++q) s -= a[q] * Lt[k * D + q];  // Lt[k][q] = L(k,q) d_q
+    const T dk = __shfl_sync(mk, s, k, 16);
+    const T rk = T(1) / dk;
+    if (l == k) dl = dk;
+    if (l > k && l < D) {
+      Lt[l * D + k] = s;  // unscaled L(l,k) d_k, broadcast in the later steps
+      a[k] = s * rk;      // L(l,k)
+    }
+    __syncwarp(mk);
+  }
+  // L y = b (column sweep), z = y / d
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    const T yq = __shfl_sync(mk, rhs, q, 16);
+    if (l > q && l < D) rhs -= a[q] * yq;
+  }
+  rhs = rhs / dl;
+  // unit-lower rows to shared memory for the transposed sweep
+  if (l < D) {
+#pragma unroll
+    for (int q = 0; q < D; ++q) Lt[l * D + q] = (q < l) ? a[q] : T(0);
+  }
+  __syncwarp(mk);
+#pragma unroll
+  for (int j = D - 1; j >= 0; --j) {
+    const T xj = __shfl_sync(mk, rhs, j, 16);
+    if (l < j) rhs -= Lt[j * D + l] * xj;
+  }
+}
+
+template <class T, int NB, int MB>
+__global__ void __launch_bounds__(16 * kPrHw) k_reconstruct_primal_hw(PrimalParams<T> p) {
+  __shared__ __align__(16) T tiles[kPrHw][NB * NB];
+  const int hw = threadIdx.x >> 4, l = threadIdx.x & 15;
+  const unsigned mk = 0xffffu << (threadIdx.x & 16);
+  const int N = p.N, K = N + 1;
+  // half-warp tasks: [0, B*K) state solves, then [B*K, B*K + B*N) control
+  // solves; the two half-warps of a warp always run the same kind (no
+  // divergence between the n- and m-sized code paths)
+  const long long nx = static_cast<long long>(p.B) * K;
+  const long long nxp = (nx + 1) & ~1LL;  // state tasks padded to whole warps
+  const long long g = static_cast<long long>(blockIdx.x) * kPrHw + hw;
+  int sys, k, blk;
+  if (g < nxp) {
+    if (g >= nx) return;
+    blk = 0;
+    sys = static_cast<int>(g / K);
+    k = static_cast<int>(g % K);
+  } else {
+    const long long u = g - nxp;
+    if (MB == 0 || u >= static_cast<long long>(p.B) * N) return;
+    blk = 1;
+    sys = static_cast<int>(u / N);
+    k = static_cast<int>(u % N);
+  }
+  T* Lt = tiles[hw];
+  const T* lam = p.lambda + static_cast<size_t>(sys) * K * NB;
+  const T* lam1 = lam + static_cast<size_t>(k + 1) * NB;
+  const size_t pd = static_cast<size_t>(K) * NB + static_cast<size_t>(N) * MB;
+  T* dz = p.dz + static_cast<size_t>(sys) * pd + static_cast<size_t>(k) * (NB + MB);
+  if (blk == 0) {
+    const int lr = l < NB ? l : NB - 1;
+    // Q_k through the tile with coalesced 16-lane loads (each sector fetched once)
+    const T* Q = p.Q + (static_cast<size_t>(sys) * K + k) * NB * NB;
+#pragma unroll
+    for (int i = l; i < NB * NB; i += 16) Lt[i] = __ldg(Q + i);
+    __syncwarp(mk);
+    T a[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) a[j] = Lt[lr * NB + j];
+    __syncwarp(mk);
+    T at = T(0);
+    if (k < N) {  // (A_k' lambda_{k+1})_l = sum_j A_k(j, l) lambda_{k+1, j}
+      const T* A = p.A + (static_cast<size_t>(sys) * N + k) * NB * NB;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) at += __ldg(A + j * NB + lr) * __ldg(lam1 + j);
+    }
+    T rhs = -(__ldg(p.q + (static_cast<size_t>(sys) * K + k) * NB + lr) +
+              __ldg(lam + static_cast<size_t>(k) * NB + lr) - at);
+    hw_ldlt_solve<T, NB>(a, rhs, Lt, l, mk);
+    if (l < NB) dz[l] = rhs;
+  } else {
+    const int lr = l < MB ? l : MB - 1;
+    const T* Rm = p.R + (static_cast<size_t>(sys) * N + k) * MB * MB;
+#pragma unroll
+    for (int i = l; i < MB * MB; i += 16) Lt[i] = __ldg(Rm + i);
+    __syncwarp(mk);
+    T a[MB];
+#pragma unroll
+    for (int j = 0; j < MB; ++j) a[j] = Lt[lr * MB + j];
+    __syncwarp(mk);
+    const T* Bm = p.B_ + (static_cast<size_t>(sys) * N + k) * NB * MB;
+    T bt = T(0);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) bt += __ldg(Bm + j * MB + lr) * __ldg(lam1 + j);
+    T rhs = -(__ldg(p.r + (static_cast<size_t>(sys) * N + k) * MB + lr) - bt);
+    hw_ldlt_solve<T, MB>(a, rhs, Lt, l, mk);
+    if (l < MB) dz[NB + l] = rhs;
+  }
+}
+}  // namespace
+
 template <class T>
 cudaError_t launch_reconstruct_primal(const PrimalParams<T>& p, cudaStream_t st) {
   const long long tasks = static_cast<long long>(p.B) * (p.N + 1) * 2;
+  auto hw_launch = [&](auto kern) {
+    const long long nx = static_cast<long long>(p.B) * (p.N + 1);
+    const long long ht = ((nx + 1) & ~1LL) + static_cast<long long>(p.B) * p.N;
+    const long long grid = (ht + kPrHw - 1) / kPrHw;
+    kern<<<static_cast<unsigned>(grid), 16 * kPrHw, 0, st>>>(p);
+    return cudaGetLastError();
+  };
+  if (tasks / kPrHw < 0x7fffffffLL) {
+    if constexpr (sizeof(T) == 8) {
+      if (p.n == 14 && p.m == 7) return hw_launch(k_reconstruct_primal_hw<T, 14, 7>);
+    } else {
+      if (p.n == 12 && p.m == 4) return hw_launch(k_reconstruct_primal_hw<T, 12, 4>);
+    }
+  }
   const long long grid = (tasks + kPrWarps - 1) / kPrWarps;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
   k_reconstruct_primal<T><<<static_cast<unsigned>(grid), 32 * kPrWarps, 0, st>>>(p);
