@@ -309,3 +309,24 @@ def test_one_cta_fused_kernel_warm_start_cap_and_errors(api, orc, env):
     bad.Q[4][33] = -np.eye(14)  # knot 33: second half-warp pass (r = 1)
     with pytest.raises(RuntimeError, match="build_schur: Q at knot 33 is not positive definite"):
         api.solve_batched(bad, PrecondKind.symmetric_stair, cfg=cfg)
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_solve_batched_multi_shards_match_single_device(api, devices):
+    """K4 host driver (b2p_solve_batched_multi): contiguous batch-index shards,
+    one host thread + context per listed device. Listing device 0 several times
+    runs the shards concurrently on the one GPU of this box, exercising the
+    sharding, per-thread contexts and error/report merging; every system's
+    result must equal the single-call batched solve bitwise (one CTA per
+    system, no cross-system arithmetic)."""
+    B = 37  # ragged shards
+    kb = api.random_kkt_batch(4242, B, 63, 14, 7)
+    cfg = PcgConfig(epsilon=1e-8)
+    lam1, rep1 = api.solve_batched(kb, PrecondKind.symmetric_stair, cfg=cfg)
+    lamm, repm = api.solve_batched_multi(devices, kb, PrecondKind.symmetric_stair, cfg=cfg)
+    assert np.array_equal(lam1, lamm)
+    assert [r.iterations for r in rep1] == [r.iterations for r in repm]
+    bad = api.random_kkt_batch(4243, B, 63, 14, 7)
+    bad.R[30][12] = -np.eye(7)  # system 30 lands in the last shard
+    with pytest.raises(RuntimeError, match="build_schur: R at knot 12 is not positive definite"):
+        api.solve_batched_multi(devices, bad, PrecondKind.symmetric_stair, cfg=cfg)
