@@ -102,7 +102,27 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
   return s;
 }
 
-template <class T, int MODE>
+// row . vector dot product: compile-time n (fully unrolled, two interleaved
+// partial sums) or the runtime-n loop
+template <int NBC, class T>
+__device__ __forceinline__ T dotn(const T* a, const T* x, int nb) {
+  if constexpr (NBC > 0) {
+    T s0 = T(0), s1 = T(0);
+#pragma unroll
+    for (int j = 0; j + 1 < NBC; j += 2) {
+      s0 += a[j] * x[j];
+      s1 += a[j + 1] * x[j + 1];
+    }
+    if constexpr (NBC & 1) s0 += a[NBC - 1] * x[NBC - 1];
+    return s0 + s1;
+  } else {
+    T s = T(0);
+    for (int j = 0; j < nb; ++j) s += a[j] * x[j];
+    return s;
+  }
+}
+
+template <class T, int MODE, int NBC = 0>
 struct Solver {
   const PcgParams<T>& p;
   int K, nb, nn, sys, rank;
@@ -190,21 +210,18 @@ struct Solver {
   __device__ __forceinline__ T bt_row(const T* M, const T* x, int b, int i) const {
     const T* D = M + nn + i * nb;
     const T* xb = x + vi(b);
-    T sd = T(0);
-    for (int j = 0; j < nb; ++j) sd += D[j] * xb[j];
+    T sd = dotn<NBC>(D, xb, nb);
     T out = sd;
     if (b > 0) {
       const T* Lr = M + i * nb;
       const T* xl = xb - nb;
-      T sl = T(0);
-      for (int j = 0; j < nb; ++j) sl += Lr[j] * xl[j];
+      T sl = dotn<NBC>(Lr, xl, nb);
       out += sl;
     }
     if (b + 1 < K) {
       const T* Rr = M + 2 * nn + i * nb;
       const T* xr = xb + nb;
-      T sr = T(0);
-      for (int j = 0; j < nb; ++j) sr += Rr[j] * xr[j];
+      T sr = dotn<NBC>(Rr, xr, nb);
       out += sr;
     }
     return out;
@@ -218,15 +235,13 @@ struct Solver {
     if (b > 0) {
       const T* Lr = M + i * nb;
       const T* xl = x + vi(b - 1);
-      T sl = T(0);
-      for (int j = 0; j < nb; ++j) sl += -Lr[j] * xl[j];
+      T sl = -dotn<NBC>(Lr, xl, nb);
       out += sl;
     }
     if (b + 1 < K) {
       const T* Rr = M + 2 * nn + i * nb;
       const T* xr = x + vi(b + 1);
-      T sr = T(0);
-      for (int j = 0; j < nb; ++j) sr += -Rr[j] * xr[j];
+      T sr = -dotn<NBC>(Rr, xr, nb);
       out += sr;
     }
     return out;
@@ -235,9 +250,7 @@ struct Solver {
   __device__ __forceinline__ T theta_row(const T* x, int b, int i) const {
     const T* Ti = Tirow(b) + i * nb;
     const T* xb = x + vi(b);
-    T s = T(0);
-    for (int j = 0; j < nb; ++j) s += Ti[j] * xb[j];
-    return s;
+    return dotn<NBC>(Ti, xb, nb);
   }
 
   __device__ __forceinline__ int shrink_lo(int a) const { return a > 0 ? a + 1 : 0; }
@@ -296,15 +309,13 @@ struct Solver {
       if (b > 0) {
         const T* Lr = M + i * nb;
         const T* tl = vt + vi(b - 1);
-        T sl = T(0);
-        for (int j = 0; j < nb; ++j) sl += Lr[j] * tl[j];
+        T sl = dotn<NBC>(Lr, tl, nb);
         v -= sl;
       }
       if (b + 1 < K) {
         const T* Rr = M + 2 * nn + i * nb;
         const T* tr = vt + vi(b + 1);
-        T sr = T(0);
-        for (int j = 0; j < nb; ++j) sr += Rr[j] * tr[j];
+        T sr = dotn<NBC>(Rr, tr, nb);
         v -= sr;
       }
       u[vi(b) + i] = v;
@@ -361,7 +372,7 @@ struct Solver {
   }
 };
 
-template <class T, int MODE, int SYNC>
+template <class T, int MODE, int SYNC, int NBC>
 __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int sys, rank;
@@ -373,7 +384,7 @@ __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
     rank = blockIdx.x % p.G;
   }
   if (p.errkey && p.errkey[sys] < 0x7f7f7f7f) return;  // formation failed (K1)
-  Solver<T, MODE> s(p, sys, rank, smem_raw);
+  Solver<T, MODE, NBC> s(p, sys, rank, smem_raw);
   unsigned gtarget = 0;  // grid-barrier generation (kSyncGrid)
   const int K = p.K, nb = p.nb;
   const size_t D = static_cast<size_t>(K) * nb;
@@ -567,10 +578,10 @@ __global__ void __launch_bounds__(512) k_pcg(PcgParams<T> p) {
   }
 }
 
-template <class T, int MODE, int SYNC>
+template <class T, int MODE, int SYNC, int NBC>
 cudaError_t launch_mode(const PcgParams<T>& p, cudaStream_t st) {
   const size_t smem = pcg_smem_bytes(p);
-  auto kern = k_pcg<T, MODE, SYNC>;
+  auto kern = k_pcg<T, MODE, SYNC, NBC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -603,18 +614,30 @@ cudaError_t launch_mode(const PcgParams<T>& p, cudaStream_t st) {
   }
 }
 
+template <class T, int NBC>
+cudaError_t launch_nb(const PcgParams<T>& p, cudaStream_t st) {
+  if (p.mode == kModeFused) {
+    if (p.sync == kSyncCta) return launch_mode<T, kModeFused, kSyncCta, NBC>(p, st);
+    if (p.sync == kSyncCluster) return launch_mode<T, kModeFused, kSyncCluster, NBC>(p, st);
+    return launch_mode<T, kModeFused, kSyncGrid, NBC>(p, st);
+  }
+  if (p.sync == kSyncCta) return launch_mode<T, kModeExplicit, kSyncCta, NBC>(p, st);
+  if (p.sync == kSyncCluster) return launch_mode<T, kModeExplicit, kSyncCluster, NBC>(p, st);
+  return launch_mode<T, kModeExplicit, kSyncGrid, NBC>(p, st);
+}
+
 }  // namespace
 
+// compile-time block dim for the BASELINE shapes (c1/c2/c4: n = 14 fp64,
+// c3: n = 12 fp32), the runtime-n kernel otherwise
 template <class T>
 cudaError_t launch_pcg(const PcgParams<T>& p, cudaStream_t st) {
-  if (p.mode == kModeFused) {
-    if (p.sync == kSyncCta) return launch_mode<T, kModeFused, kSyncCta>(p, st);
-    if (p.sync == kSyncCluster) return launch_mode<T, kModeFused, kSyncCluster>(p, st);
-    return launch_mode<T, kModeFused, kSyncGrid>(p, st);
+  if constexpr (sizeof(T) == 8) {
+    if (p.nb == 14) return launch_nb<T, 14>(p, st);
+  } else {
+    if (p.nb == 12) return launch_nb<T, 12>(p, st);
   }
-  if (p.sync == kSyncCta) return launch_mode<T, kModeExplicit, kSyncCta>(p, st);
-  if (p.sync == kSyncCluster) return launch_mode<T, kModeExplicit, kSyncCluster>(p, st);
-  return launch_mode<T, kModeExplicit, kSyncGrid>(p, st);
+  return launch_nb<T, 0>(p, st);
 }
 
 template cudaError_t launch_pcg<double>(const PcgParams<double>&, cudaStream_t);
