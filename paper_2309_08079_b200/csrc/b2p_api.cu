@@ -368,6 +368,37 @@ void launch_form(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, T* S, T*
   f.theta_inv = ti;
   f.errkey = errkey;
   CK(cudaMemsetAsync(errkey, 0x7f, sizeof(int) * B, st));  // 0x7f7f7f7f: see below
+  const int K = k->N + 1;
+  if (env_int("B2P_FUSED", 1) && fused_supported<T>(K, k->n, k->m, kSymStair)) {
+    // the fused kernel's formation phase (shared Q_k^-1, half-warp rows) in
+    // formation-only mode writes S / gamma / theta^-1 in the reference layout
+    const int grid = std::max(1, std::min(B, c->sm_count));
+    FusedParams<T> g{};
+    g.B = B;
+    g.K = K;
+    g.kind = kSymStair;
+    g.Q = f.Q;
+    g.q = f.q;
+    g.R = f.R;
+    g.r = f.r;
+    g.A = f.A;
+    g.Bm = f.Bm;
+    g.e = f.e;
+    g.x_s = f.x_s;
+    g.x0 = f.x0;
+    g.slot = static_cast<T*>(ws_get(c, "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, k->n, k->m)));
+    g.errkey = errkey;
+    g.out = static_cast<SysOut*>(ws_get(c, "form_out", sizeof(SysOut) * B));
+    g.S_out = S;
+    g.gamma_out = gamma;
+    g.theta_out = ti;
+    g.form_only = 1;
+    g.max_iter = 1;
+    CK(cudaMemsetAsync(S, 0, sizeof(T) * static_cast<size_t>(B) * K * 3 * k->n * k->n, st));
+    CK(launch_fused<T>(g, grid, st));
+    c->launches++;
+    return;
+  }
   CK(launch_build_schur<T>(f, st));
   c->launches++;
 }

@@ -342,6 +342,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
           for (int i = 0; i < NB; ++i) gT[i * NB + l] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
           gG[l] = -((xs[l] - x0[l]) + sqq[l]);
+          if (p.form_only) {
+            T* So = p.S_out + static_cast<size_t>(sys) * K * 3 * nn;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+              So[nn + i * NB + l] = sQi[i * NB + l];
+              p.theta_out[static_cast<size_t>(sys) * K * nn + i * NB + l] =
+                  T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
+            }
+            p.gamma_out[static_cast<size_t>(sys) * K * NB + l] = gG[l];
+          }
         }
       }
       const int k = b - 1;
@@ -408,6 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int i = 0; i < NB; ++i) {
           tW[i * LD + l] = x[i];
           if (wr) gL[static_cast<size_t>(b) * nn + i * NB + l] = -x[i];
+          if (wr && p.form_only)  // S.left(b) = phi (schur.cpp:74)
+            p.S_out[(static_cast<size_t>(sys) * K + b) * 3 * nn + i * NB + l] = -x[i];
         }
 #pragma unroll
         for (int q = 0; q < MB; ++q) tBR[l * LDM + q] = br[q];
@@ -418,6 +430,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int j = 0; j < NB; ++j) lrow[j] = -tW[lr * LD + j];
         tm_st_row14(colL(r), lrow);
+        if (wr && lact && p.form_only) {  // S.right(b-1) = phi' (schur.cpp:74)
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            p.S_out[((static_cast<size_t>(sys) * K + b - 1) * 3 + 2) * nn + j * NB + l] = lrow[j];
+        }
       }
       // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
 #pragma unroll
@@ -437,7 +454,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int q = 0; q < MB; ++q) brr += brow[q] * srr[k * 8 + q];
         const T zeta = (-aqq - brr) + sqq[(k + 1) * 16 + lr];
-        if (wr && lact) gG[static_cast<size_t>(b) * NB + l] = -(-__ldg(es + k * NB + l) + zeta);
+        if (wr && lact) {
+          const T g = -(-__ldg(es + k * NB + l) + zeta);
+          gG[static_cast<size_t>(b) * NB + l] = g;
+          if (p.form_only) p.gamma_out[(static_cast<size_t>(sys) * K + b) * NB + l] = g;
+        }
       }
       hw_symmetrize_col<T, NB, LD, true>(tW, l, x);  // theta (schur.cpp:67)
       {  // row l of D_b = theta (row 0: Q_0^-1, schur.cpp:53) -> TMEM
@@ -445,6 +466,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) drow[i] = (b0 == 0) ? sQi[lr * NB + i] : x[i];
         tm_st_row14(colD(r), drow);
+        if (wr && lact && p.form_only) {  // S.diag(b) = theta (schur.cpp:73)
+#pragma unroll
+          for (int i = 0; i < NB; ++i)
+            p.S_out[((static_cast<size_t>(sys) * K + b) * 3 + 1) * nn + i * NB + l] = drow[i];
+        }
       }
       // theta^-1 (schur.cpp:75): x holds row l of the symmetric theta
       {
@@ -456,7 +482,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       }
       if (wr && lact) {
 #pragma unroll
-        for (int i = 0; i < NB; ++i) gT[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
+        for (int i = 0; i < NB; ++i) {
+          gT[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
+          if (p.form_only)  // theta_inv[b] (bitwise symmetric: row = column)
+            p.theta_out[(static_cast<size_t>(sys) * K + b) * nn + i * NB + l] = x[i];
+        }
       }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
@@ -475,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       continue;
     }
     if (tid == 0 && p.errkey) p.errkey[sys] = 0x7f7f7f7f;
+    if (p.form_only) continue;  // build_schur only
 
     // ================================================================ P
     // stage L, D (contiguous in the slot and in shared memory) with one TMA

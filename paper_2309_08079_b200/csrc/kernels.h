@@ -76,6 +76,12 @@ struct FusedParams {
   double epsilon;
   int max_iter;
   unsigned long long* timing;  // optional [B][8] globaltimer stamps per phase (debug)
+  // formation only (build_schur): write S [B][K][3][n][n] (zeroed pads), gamma
+  // [B][K n], theta^-1 [B][K][n][n] in the reference layout and skip the PCG
+  T* S_out;
+  T* gamma_out;
+  T* theta_out;
+  int form_only;
 };
 template <class T> bool fused_supported(int K, int n, int m, int kind);
 template <class T> size_t fused_slot_elems(int K, int n, int m);

@@ -77,6 +77,26 @@ def main():
     for rp in (1, 2):
         out[f"c1_symstair_1e-8_fusedgrid_rp{rp}"] = timed(
             k1, PrecondKind.symmetric_stair, 1e-8, env={"B2P_FG": "1", "B2P_FG_RP": str(rp)})
+    # build_schur API (host buffers in/out, wall time incl. copies): fused formation
+    # kernel in formation-only mode vs the split K1 kernel
+    for tag, envv in (("fused_formation", {}), ("split_K1", {"B2P_FUSED": "0"})):
+        saved = {kk: os.environ.get(kk) for kk in envv}
+        os.environ.update(envv)
+        try:
+            for _ in range(3):
+                api.build_schur(k1)
+            ts = []
+            for _ in range(20):
+                t0 = time.perf_counter()
+                api.build_schur(k1)
+                ts.append((time.perf_counter() - t0) * 1e6)
+            out[f"c1_build_schur_api_{tag}_us"] = statistics.median(ts)
+        finally:
+            for kk, vv in saved.items():
+                if vv is None:
+                    os.environ.pop(kk, None)
+                else:
+                    os.environ[kk] = vv
     k2 = orc.random_kkt(2, 127, 14, 7)
     for kind, name in [(PrecondKind.block_jacobi, "jacobi"), (PrecondKind.stair, "stair"),
                        (PrecondKind.symmetric_stair, "symstair")]:
