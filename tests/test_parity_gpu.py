@@ -330,3 +330,32 @@ def test_solve_batched_multi_shards_match_single_device(api, devices):
     bad.R[30][12] = -np.eye(7)  # system 30 lands in the last shard
     with pytest.raises(RuntimeError, match="build_schur: R at knot 12 is not positive definite"):
         api.solve_batched_multi(devices, bad, PrecondKind.symmetric_stair, cfg=cfg)
+
+
+@pytest.mark.parametrize("shape", [(63, 14, 7), (63, 12, 4), (31, 6, 3)])
+def test_fp32_batched_solves_match_fp32_oracle(api, orc, shape):
+    """fp32 batches on every path the dispatcher picks for them (cluster kernel
+    for n12/m4, split K1 + K3 otherwise) against the fp32 oracle (1e-5)."""
+    N, n, m = shape
+    B = 9
+    kb = api.random_kkt_batch(5150 + n, B, N, n, m)
+    cfg = PcgConfig(epsilon=1e-6)
+    lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, cfg=cfg, dtype=np.float32)
+    assert lam.dtype == np.float32
+    for i in (0, 4, 8):
+        want = orc.solve(kb.system(i), PrecondKind.symmetric_stair, cfg=cfg, dtype=np.float32)
+        assert reps[i].iterations == want.report.iterations
+        assert rel_inf_error(lam[i], want.lambda_) <= TOL32
+
+
+def test_max_iter_zero_means_dim_and_trace_lengths(api, orc):
+    """resolve_max_iter (pcg.cpp:49-51): max_iter = 0 -> dim; the trace holds
+    iterations 1..i (pcg.cpp:102) on the fused one-CTA path."""
+    kkt = orc.random_kkt(11, 31, 14, 7)
+    cfg = PcgConfig(epsilon=1e-8, max_iter=0, collect_trace=True)
+    got = api.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    want = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    assert got.report.iterations == want.report.iterations
+    assert len(got.report.trace) == got.report.iterations == len(want.report.trace)
+    np.testing.assert_allclose(got.report.trace, want.report.trace, rtol=1e-8)
+    assert got.report.trace[-1] == got.report.exit_eta
