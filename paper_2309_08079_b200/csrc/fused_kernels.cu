@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   const bool lact = l < NB;
   T* smem = reinterpret_cast<T*>(smem_raw);
   // PCG layout
-  T* sL = smem;                          // [K][NB][NB] (column products)
+  // PCG layout starts after the formation's Q region: while system s runs its
+  // PCG, the Q_k and q_k of the CTA's next system are TMA-prefetched into
+  // [0, K*NN) and the q region (both untouched by the PCG phase)
+  T* sL = smem + static_cast<size_t>(K) * NN;  // [K][NB][NB] (column products)
   T* sp = sL + static_cast<size_t>(K) * NN;  // [K][NB]
   T* st = sp + K * NB;
   T* su = st + K * NB;
@@ -200,11 +203,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   T* srr = smem + FL::orr(K);   // [N][8]   R_k^-1 r_k
   __shared__ int s_err;
   __shared__ __align__(8) unsigned long long s_mbar;  // TMA staging barrier
+  __shared__ __align__(8) unsigned long long s_mbar2;  // next system's Q prefetch
   const unsigned mbar_addr = static_cast<unsigned>(__cvta_generic_to_shared(&s_mbar));
-  unsigned mbar_phase = 0;
+  const unsigned mbar2_addr = static_cast<unsigned>(__cvta_generic_to_shared(&s_mbar2));
+  unsigned mbar_phase = 0, mbar2_phase = 0;
+  bool qpre = false;  // this system's Q_k / q_k already on their way (prefetched)
   __shared__ unsigned s_taddr;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar_addr) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar2_addr) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if ((tid >> 5) == 0) {  // warp 0 owns the whole TMEM of the SM (one CTA per SM)
@@ -258,17 +265,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // row, schur.cpp:49-51; same arithmetic). All Q_k arrive in one TMA bulk
     // copy (sQi) and are inverted in place; lanes read their rows from smem.
     T* sq = smem + FL::osq(K);  // q_k of every knot (for Q_k^-1 q_k)
-    if (tid == 0) {
-      const unsigned bq = static_cast<unsigned>(sizeof(T) * K * nn);
-      const unsigned bv = static_cast<unsigned>(sizeof(T) * K * NB);
-      asm volatile("fence.proxy.async;\n" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
-                   "r"(bq + bv)
-                   : "memory");
-      tma_copy_1d(sQi, Qs, bq, mbar_addr);
-      tma_copy_1d(sq, qs, bv, mbar_addr);
+    if (qpre) {
+      mbar_wait(mbar2_addr, mbar2_phase);  // prefetched during the previous PCG
+    } else {
+      if (tid == 0) {
+        const unsigned bq = static_cast<unsigned>(sizeof(T) * K * nn);
+        const unsigned bv = static_cast<unsigned>(sizeof(T) * K * NB);
+        asm volatile("fence.proxy.async;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
+                     "r"(bq + bv)
+                     : "memory");
+        tma_copy_1d(sQi, Qs, bq, mbar_addr);
+        tma_copy_1d(sq, qs, bv, mbar_addr);
+      }
+      mbar_wait(mbar_addr, mbar_phase);
     }
-    mbar_wait(mbar_addr, mbar_phase);
+    qpre = false;
     // Both half-warps of a warp always run the same code (out-of-range knots
     // recompute a clamped duplicate and store nothing), so every shuffle and
     // sync below uses the full-warp mask.
@@ -515,6 +527,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       const unsigned bytes = static_cast<unsigned>(sizeof(T) * K * NN);
       if (tid == 0) tma_load_1d(sL, gL, bytes, mbar_addr);
       const int nsys = sys + gridDim.x;
+      if (nsys < p.B) {  // next system's Q_k, q_k straight into the formation's regions
+        if (tid == 0) {
+          const unsigned bq = static_cast<unsigned>(sizeof(T) * K * nn);
+          const unsigned bv = static_cast<unsigned>(sizeof(T) * K * NB);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar2_addr),
+                       "r"(bq + bv)
+                       : "memory");
+          tma_copy_1d(sQi, p.Q + static_cast<size_t>(nsys) * K * nn, bq, mbar2_addr);
+          tma_copy_1d(smem + FL::osq(K), p.q + static_cast<size_t>(nsys) * K * NB, bv, mbar2_addr);
+        }
+        qpre = true;
+      }
       if (nsys < p.B && tid < 9) {
         // per-field contiguous ranges of the next system (16-byte aligned inside)
         const T* base[9] = {p.Q, p.q, p.R, p.r, p.A, p.Bm, p.e, p.x_s, p.x0};
@@ -769,7 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 template <class T, int NB, int MB>
 size_t fused_smem_bytes(int K) {
   using FL = FLayout<T, NB, MB>;
-  const size_t pcg = sizeof(T) * (static_cast<size_t>(K) * NB * NB + 3 * K * NB + 64);
+  const size_t pcg = sizeof(T) * (static_cast<size_t>(2) * K * NB * NB + 3 * K * NB + 64);
   const size_t form = sizeof(T) * static_cast<size_t>(FL::total(K));
   return std::max(pcg, form);
 }
