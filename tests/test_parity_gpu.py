@@ -359,3 +359,24 @@ def test_max_iter_zero_means_dim_and_trace_lengths(api, orc):
     assert len(got.report.trace) == got.report.iterations == len(want.report.trace)
     np.testing.assert_allclose(got.report.trace, want.report.trace, rtol=1e-8)
     assert got.report.trace[-1] == got.report.exit_eta
+
+
+def test_c4_persistent_ctas_over_several_systems(api, orc):
+    """B > #SMs: every persistent CTA of the one-CTA kernel solves 2-3 systems
+    in turn (slot, TMEM and shared-memory reuse, the next system's Q prefetched
+    during the current PCG). Systems of the 2nd and 3rd pass against the oracle,
+    and every system equal to its own single-system batch bitwise."""
+    B = 400
+    kb = api.random_kkt_batch(6000, B, 63, 14, 7)
+    cfg = PcgConfig(epsilon=1e-8)
+    lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, cfg=cfg)
+    assert api.context().last_path() == 1
+    for i in (0, 147, 148, 200, 295, 296, 399):
+        want = orc.solve(kb.system(i), PrecondKind.symmetric_stair, cfg=cfg)
+        assert reps[i].iterations == want.report.iterations
+        assert rel_inf_error(lam[i], want.lambda_) <= TOL64
+    # the same systems as a batch of 12 (one system per CTA): bitwise equal
+    idx = [0, 1, 148, 149, 296, 297, 350, 351, 398, 399, 10, 300]
+    sub = type(kb)(kb.N, kb.n, kb.m, *[np.ascontiguousarray(a[idx]) for a in kb.arrays()])
+    lam2, _ = api.solve_batched(sub, PrecondKind.symmetric_stair, cfg=cfg)
+    assert np.array_equal(lam2, lam[idx])
