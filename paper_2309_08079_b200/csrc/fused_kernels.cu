@@ -288,14 +288,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     for (int r = 0; r < R; ++r) {
       const int k = h + r * kHalfWarps;
       // R_k row l issued before the Q_k inverse so its L2 latency is hidden
-      T ra[MB];
-      {
-        const int kc = k < N ? k : N - 1;
-        const int lm = l < MB ? l : MB - 1;
-        const T* Rr = Rs + static_cast<size_t>(kc) * mm + lm * MB;
-#pragma unroll
-        for (int i = 0; i < MB; ++i) ra[i] = __ldg(Rr + i);
-      }
       {
         const bool kv = k < K;
         const int kc = kv ? k : K - 1;
@@ -321,20 +313,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           sqq[k * 16 + l] = qq;
         }
       }
-      {
-        const bool kv = k < N;
-        T x[MB];
-        const int f = hw_spd_inverse_v2<T, MB, true>(ra, tW, tX, rd, l, x);
-        if (kv && f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
-        if (kv && l < MB) {
-          T rr = T(0);
+    }
+    {
+      // R_k^-1 of the half-warp's two knots at once (m = 7 fits 8-lane groups):
+      // lanes 0-7 knot h, lanes 8-15 knot h + 32
+      static_assert(MB <= 8, "");
+      const int sub = l >> 3, ls = l & 7;
+      const int k = h + sub * kHalfWarps;
+      const bool kv = k < N && sub < R;
+      const int kc = kv ? k : N - 1;
+      const int lm = ls < MB ? ls : MB - 1;
+      T ra[MB], x[MB];
+      const T* Rr = Rs + static_cast<size_t>(kc) * mm + lm * MB;
 #pragma unroll
-          for (int i = 0; i < MB; ++i) {
-            gR[static_cast<size_t>(k) * mm + i * MB + l] = x[i];
-            rr += x[i] * rs[k * MB + i];
-          }
-          srr[k * 8 + l] = rr;
+      for (int i = 0; i < MB; ++i) ra[i] = __ldg(Rr + i);
+      const int f = g8_spd_inverse<T, MB>(ra, tW + sub * 64, tX + sub * 64, rd + sub * 8, ls, x);
+      if (kv && f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
+      if (kv && ls < MB) {
+        T rr = T(0);
+#pragma unroll
+        for (int i = 0; i < MB; ++i) {
+          gR[static_cast<size_t>(k) * mm + i * MB + ls] = x[i];
+          rr += x[i] * rs[k * MB + i];
         }
+        srr[k * 8 + ls] = rr;
       }
     }
     __syncthreads();

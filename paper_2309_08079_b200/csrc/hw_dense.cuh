@@ -269,5 +269,55 @@ __device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd
   return fail;
 }
 
+
+// hw_spd_inverse_v2 for N <= 8 on 8-lane groups: a half-warp inverts two
+// independent matrices at once (lanes 0-7 and 8-15). l = lane & 7; every lane
+// of the warp must call it (full-warp mask, width-8 shuffles); Lr / LiT / rd
+// are the calling group's own tiles.
+template <class T, int N>
+__device__ __forceinline__ int g8_spd_inverse(T (&a)[N], T* Lr, T* LiT, T* rd, int l, T (&x)[N]) {
+  static_assert(N <= 8, "8-lane groups");
+  int fail = -1;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    T s = a[k];
+#pragma unroll
+    for (int q = 0; q < k; ++q) s -= a[q] * Lr[k * N + q];
+    T piv = __shfl_sync(FULL, s, k, 8);
+    const bool bad = piv <= T(0);  // x <= 0 fails, NaN passes (Eigen LLT)
+    fail = (bad && fail < 0) ? k : fail;
+    piv = bad ? T(1) : piv;
+    const T r = rsqrt(piv);
+    const T val = (l == k ? piv : s) * r;
+    const bool own = l >= k && l < N;
+    a[k] = own ? val : a[k];
+    if (own) Lr[l * N + k] = val;
+    if (l == k) rd[k] = r;
+    __syncwarp();
+  }
+  T y[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T s = (i == l) ? T(1) : T(0);
+#pragma unroll
+    for (int q = 0; q < i; ++q) s -= Lr[i * N + q] * y[q];
+    y[i] = s * rd[i];
+  }
+  if (l < N) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) LiT[l * N + q] = y[q];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T s = T(0);
+#pragma unroll
+    for (int q = i; q < N; ++q) s += LiT[i * N + q] * y[q];
+    x[i] = s;
+  }
+  __syncwarp();
+  return fail;
+}
+
 }  // namespace hwd
 }  // namespace b2p
