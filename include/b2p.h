@@ -229,6 +229,16 @@ int b2p_reconstruct_primal_batched_device(b2p_ctx* ctx, int dtype, int batch,
                                           const b2p_kkt* kkt_batch_dev, const void* lambda_dev,
                                           void* dz_dev, b2p_error* err);
 
+/* ---- the SQP linear step (sqp.cpp:171-176): build_schur ->
+ * build_preconditioner -> pcg_solve_auto(lambda0) -> reconstruct_primal(lambda)
+ * on ONE upload of the knots: the fused solve and the primal kernel run
+ * back to back on the context stream, then lambda_out ((N+1) n) and dz_out
+ * ((N+1) n + N m) come back together. Errors as b2p_solve; dz is produced only
+ * on success (the reference's exception leaves no dz either). */
+int b2p_sqp_step(b2p_ctx* ctx, int dtype, const b2p_kkt* kkt, int kind, int order,
+                 const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out, void* dz_out,
+                 b2p_solve_report* report, double* trace, b2p_error* err);
+
 /* Device time (ms) of the most recent solve kernels on this context. */
 int b2p_ctx_last_solve_ms(b2p_ctx* ctx, float* ms);
 /* Per-kernel split of the most recent fused solve: ms[0] = K1 Schur

@@ -469,6 +469,32 @@ inline Vector reconstruct_primal(const KKTSystem& kkt, const Vector& lambda) {
   return dz;
 }
 
+/// The SQP linear step (sqp.cpp:171-176) in one library call: fused
+/// build_schur -> build_preconditioner -> pcg_solve_auto(lambda0), then
+/// reconstruct_primal on the knots already resident on the device.
+struct SqpStepResult {
+  PcgResult pcg;
+  Vector dz;
+};
+inline SqpStepResult sqp_step(const KKTSystem& kkt, PrecondKind kind, int order,
+                              const PcgConfig& cfg, const Vector& lambda0) {
+  const PackedKKT p = pack(kkt);
+  const b2p_kkt v = p.view(kkt.N, kkt.n, kkt.m);
+  const b2p_pcg_config c = detail::to_c(cfg);
+  SqpStepResult out;
+  out.pcg.lambda.resize(static_cast<size_t>(kkt.dual_dim()));
+  out.dz.resize(static_cast<size_t>(kkt.N + 1) * kkt.n + static_cast<size_t>(kkt.N) * kkt.m);
+  std::vector<double> trace(static_cast<size_t>(cfg.max_iter > 0 ? cfg.max_iter : kkt.dual_dim()) + 1);
+  b2p_solve_report rep{};
+  b2p_error e{};
+  detail::raise(b2p_sqp_step(detail::context(), B2P_F64, &v, static_cast<int>(kind), order, &c,
+                             lambda0.empty() ? nullptr : lambda0.data(), out.pcg.lambda.data(),
+                             out.dz.data(), &rep, trace.data(), &e),
+                e);
+  out.pcg.report = detail::from_c(rep, trace);
+  return out;
+}
+
 }  // namespace trajopt_b200
 
 #if defined(__has_include)

@@ -386,6 +386,27 @@ def reconstruct_primal(kkt: KKTSystem, lam, dtype=np.float64) -> np.ndarray:  # 
     return dz
 
 
+def sqp_step(kkt: KKTSystem, kind=PrecondKind.symmetric_stair, order: int = 1,
+             cfg: PcgConfig | None = None, lambda0=None, dtype=np.float64):
+    """The SQP linear step (sqp.cpp:171-176) on one upload: fused solve, then
+    reconstruct_primal on the resident knots. Returns (PcgResult, dz)."""
+    cfg = cfg or PcgConfig()
+    dt = np.dtype(dtype)
+    k = kkt.astype(dt)
+    D = k.dual_dim()
+    lam = np.zeros(D, dtype=dt)
+    dz = np.zeros(k.primal_dim(), dtype=dt)
+    l0 = None if lambda0 is None else _arr(lambda0, dt)
+    rep = _abi.SolveReportC()
+    trace = np.zeros(max(1, _max_iter(cfg, D)))
+    err = _abi.ErrorC()
+    c = cfg.to_c()
+    _check(load().b2p_sqp_step(context().handle, _dt(dt), C.byref(k.to_c()), int(kind),
+                               int(order), C.byref(c), _ptr(l0), _ptr(lam), _ptr(dz),
+                               C.byref(rep), _ptr(trace), C.byref(err)), err)
+    return PcgResult(lam, SolveReport.from_c(rep, trace)), dz
+
+
 def reconstruct_primal_batched_device(kkt_dev: KKTSystem, lambda_ptr: int, dz_ptr: int,
                                       batch: int, dtype=np.float64, ctx: Context | None = None):
     """Device-resident batch (tensors with .data_ptr()); no host sync."""

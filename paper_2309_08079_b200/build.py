@@ -74,6 +74,24 @@ def build_adapter_test(force: bool = False) -> str:
     return out
 
 
+def build_sqp_test(force: bool = False) -> str:
+    """g++ the SQP / NMPC caller tests (tests/cpp/test_sqp.cpp) against libb2p.so.
+    The test links the CPU oracle header as its checker (test infrastructure)."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "tests", "cpp", "test_sqp.cpp")
+    hdrs = [os.path.join(root, "include", h) for h in ("trajopt_b200.hpp", "trajopt_b200_sqp.hpp")]
+    hdrs.append(os.path.join(root, "oracle", "trajopt_oracle.hpp"))
+    out = os.path.join(root, "build", "test_sqp")
+    if not force and not _stale(out, [src, LIB] + hdrs):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++20", "-O2", "-Wall", "-pthread",
+                           "-I", os.path.join(root, "include"), "-I", os.path.join(root, "oracle"),
+                           src, "-o", out, "-L", HERE, "-lb2p",
+                           "-Wl,-rpath,$ORIGIN/../paper_2309_08079_b200"])
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)

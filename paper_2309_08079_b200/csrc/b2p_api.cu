@@ -307,30 +307,53 @@ struct KktDev {
 
 // Upload `count` systems starting at `first` from a host batch into one
 // contiguous device block; returns per-array device pointers.
-KktDev upload_kkt(b2p_ctx* c, const b2p_kkt* k, size_t esz, int first, int count, void* dst,
-                  cudaStream_t st) {
-  const size_t N = k->N, n = k->n, m = k->m, K = N + 1;
-  const size_t sz[9] = {K * n * n, K * n, N * m * m, N * m, N * n * n, N * n * m, N * n, n, n};
-  const void* src[9] = {k->Q, k->q, k->R, k->r, k->A, k->B, k->e, k->x_s, k->x0};
-  const void* out[9];
-  char* d = static_cast<char*>(dst);
-  for (int a = 0; a < 9; ++a) {
-    const size_t bytes = sz[a] * esz * count;
-    if (bytes && !src[a]) throw invalid("b2p_kkt: null array");
-    if (bytes)
-      h2d(c, d, static_cast<const char*>(src[a]) + sz[a] * esz * first, bytes, st);
-    out[a] = d;
-    d += (bytes + 255) / 256 * 256;
-  }
-  return KktDev{out[0], out[1], out[2], out[3], out[4], out[5], out[6], out[7], out[8]};
-}
-
 size_t kkt_block_bytes(const b2p_kkt* k, size_t esz, int count) {
   const size_t N = k->N, n = k->n, m = k->m, K = N + 1;
   const size_t sz[9] = {K * n * n, K * n, N * m * m, N * m, N * n * n, N * n * m, N * n, n, n};
   size_t total = 0;
   for (size_t s : sz) total += (s * esz * count + 255) / 256 * 256;
   return total;
+}
+
+// Copies systems [first, first+count) of the host batch `k` into the device
+// block `dst` (laid out as kkt_block_bytes). A single system is latency-bound:
+// its nine arrays (plus an optional trailing `extra` host vector, returned in
+// *extra_dev) are packed into one pinned staging block and sent with ONE copy
+// instead of ten pageable cudaMemcpyAsync round trips. Callers synchronise the
+// stream before returning, so the staging block is free again by the next call.
+KktDev upload_kkt(b2p_ctx* c, const b2p_kkt* k, size_t esz, int first, int count, void* dst,
+                  cudaStream_t st, const void* extra = nullptr, size_t extra_bytes = 0,
+                  char** extra_dev = nullptr) {
+  const size_t N = k->N, n = k->n, m = k->m, K = N + 1;
+  const size_t sz[9] = {K * n * n, K * n, N * m * m, N * m, N * n * n, N * n * m, N * n, n, n};
+  const void* src[9] = {k->Q, k->q, k->R, k->r, k->A, k->B, k->e, k->x_s, k->x0};
+  const void* out[9];
+  char* d = static_cast<char*>(dst);
+  const bool staged = count == 1;
+  const size_t total = kkt_block_bytes(k, esz, count) + extra_bytes;
+  char* h = staged ? static_cast<char*>(hws_get(c, "up_stage", total)) : nullptr;
+  for (int a = 0; a < 9; ++a) {
+    const size_t bytes = sz[a] * esz * count;
+    if (bytes && !src[a]) throw invalid("b2p_kkt: null array");
+    const char* from = static_cast<const char*>(src[a]) + sz[a] * esz * first;
+    if (bytes) {
+      if (staged)
+        std::memcpy(h + (d - static_cast<char*>(dst)), from, bytes);
+      else
+        h2d(c, d, from, bytes, st);
+    }
+    out[a] = d;
+    d += (bytes + 255) / 256 * 256;
+  }
+  if (extra_bytes) {
+    if (staged)
+      std::memcpy(h + (d - static_cast<char*>(dst)), extra, extra_bytes);
+    else
+      h2d(c, d, extra, extra_bytes, st);
+    *extra_dev = d;
+  }
+  if (staged) h2d(c, dst, h, total, st);
+  return KktDev{out[0], out[1], out[2], out[3], out[4], out[5], out[6], out[7], out[8]};
 }
 
 KktDev dev_view(const b2p_kkt* k) {
@@ -504,12 +527,20 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
                    : nullptr;
     c->timing = f.timing;
     c->timing_n = f.timing ? B : 0;
-    CK(launch_fg<T>(f, sy, fgRp, st));
-    c->launches++;
-    c->last_path = 3;
-    c->phases = time_it;
-    if (time_it) CK(cudaEventRecord(c->ev1, st));
-    return;
+    const cudaError_t le = launch_fg<T>(f, sy, fgRp, st);
+    if (le == cudaErrorCooperativeLaunchTooLarge) {
+      // The grid did not fit co-resident (SMs taken by another context):
+      // fall through to the cluster / split paths below.
+      (void)cudaGetLastError();
+      c->fg_epoch -= need;
+    } else {
+      CK(le);
+      c->launches++;
+      c->last_path = 3;
+      c->phases = time_it;
+      if (time_it) CK(cudaEventRecord(c->ev1, st));
+      return;
+    }
   }
   const bool use_fc = fcG > 0 && env_int("B2P_FUSED", 1) &&
                       (fc_env == 1 || (fc_env == -1 && ((B == 1 && !single_short) || !one_cta_ok)));
@@ -1208,8 +1239,14 @@ int b2p_pcg_solve(b2p_ctx* c, int dtype, int K, int nb, const void* S, int kind,
 }
 
 // ---------------------------------------------------------------- fused
-int b2p_solve(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
-              const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
+}  // extern "C"
+namespace {
+template <class T>
+void primal_impl(b2p_ctx* c, int B, const b2p_kkt* k, const KktDev& kv, const void* lam, void* dz,
+                 cudaStream_t st);
+
+int solve_one(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
+              const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out, void* dz_out,
               b2p_solve_report* report, double* trace, b2p_error* err) {
   return guard(err, [&] {
     check_dtype(dtype);
@@ -1221,16 +1258,20 @@ int b2p_solve(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
     const int K = k->N + 1, n = k->n;
     const size_t D = size_t(K) * n;
     cudaStream_t st = c->stream();
-    void* in = ws_get(c, "sv_in", kkt_block_bytes(k, es, 1));
-    const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st);
+    const size_t l0b = lambda0 ? es * D : 0;
+    void* in = ws_get(c, "sv_in", kkt_block_bytes(k, es, 1) + l0b);
     char* dl0 = nullptr;
-    if (lambda0) {
-      dl0 = static_cast<char*>(ws_get(c, "sv_l0", es * D));
-      h2d(c, dl0, lambda0, es * D, st);
-    }
-    char* dl = static_cast<char*>(ws_get(c, "sv_l", es * D));
-    SysOut* dout = static_cast<SysOut*>(ws_get(c, "sv_out", sizeof(SysOut)));
-    int* ek = static_cast<int*>(ws_get(c, "sv_ek", sizeof(int)));
+    const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st, lambda0, l0b, &dl0);
+    // Outputs in one device block -> one copy back: [SysOut | key | lambda | dz].
+    const size_t P = static_cast<size_t>(K) * n + static_cast<size_t>(k->N) * k->m;
+    const size_t oKey = 256, oL = 512, oDz = oL + (es * D + 255) / 256 * 256;
+    const size_t obytes = dz_out ? oDz + es * P : oL + es * D;
+    char* dob = static_cast<char*>(ws_get(c, "sv_ob", obytes));
+    char* hob = static_cast<char*>(hws_get(c, "sv_hob", obytes));
+    char* dl = dob + oL;
+    SysOut* dout = reinterpret_cast<SysOut*>(dob);
+    int* ek = reinterpret_cast<int*>(dob + oKey);
+    static_assert(sizeof(SysOut) <= 256, "SysOut slot");
     const int mi = (cfg && cfg->max_iter > 0) ? cfg->max_iter : int(D);
     double* dtr = nullptr;
     if (trace && cfg && cfg->collect_trace)
@@ -1241,22 +1282,49 @@ int b2p_solve(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
     else
       solve_device_impl<float>(c, k, kv, 1, kind, order, cfg, dl0, dl, dout, ek, dtr, mi, st,
                                true, "sv_");
-    SysOut o;
-    int key = 0;
-    d2h(c, &o, dout, sizeof(o), st);
-    d2h(c, &key, ek, sizeof(int), st);
-    d2h(c, lambda_out, dl, es * D, st);
+    if (dz_out) {
+      // reconstruct_primal on the resident knots and multipliers. If the solve
+      // failed, dz is never handed back.
+      if (dtype == B2P_F64)
+        primal_impl<double>(c, 1, k, kv, dl, dob + oDz, st);
+      else
+        primal_impl<float>(c, 1, k, kv, dl, dob + oDz, st);
+    }
+    d2h(c, hob, dob, obytes, st);
     CK(cudaStreamSynchronize(st));
     CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    SysOut o;
+    int key = 0;
+    std::memcpy(&o, hob, sizeof(o));
+    std::memcpy(&key, hob + oKey, sizeof(int));
+    std::memcpy(lambda_out, hob + oL, es * D);
     Fail first{B2P_OK, ""};
     resolve({o}, {key}, 1, report, c->last_ms * 1e-3, &first);
     if (first.code != B2P_OK) {
       first.system = -1;
       throw first;
     }
+    if (dz_out) std::memcpy(dz_out, hob + oDz, es * P);
     if (dtr && o.trace_len > 0)
       CK(cudaMemcpy(trace, dtr, sizeof(double) * o.trace_len, cudaMemcpyDeviceToHost));
   });
+}
+}  // namespace
+extern "C" {
+
+int b2p_solve(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
+              const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
+              b2p_solve_report* report, double* trace, b2p_error* err) {
+  return solve_one(c, dtype, k, kind, order, cfg, lambda0, lambda_out, nullptr, report, trace,
+                   err);
+}
+
+int b2p_sqp_step(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
+                 const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out, void* dz_out,
+                 b2p_solve_report* report, double* trace, b2p_error* err) {
+  if (!dz_out) return guard(err, [] { throw invalid("sqp_step: null dz buffer"); });
+  return solve_one(c, dtype, k, kind, order, cfg, lambda0, lambda_out, dz_out, report, trace,
+                   err);
 }
 
 // ------------------------------------------------------------------ reconstruct_primal
@@ -1298,17 +1366,18 @@ int b2p_reconstruct_primal(b2p_ctx* c, int dtype, const b2p_kkt* k, const void* 
     const size_t es = esize(dtype);
     const size_t P = static_cast<size_t>(k->N + 1) * k->n + static_cast<size_t>(k->N) * k->m;
     cudaStream_t st = c->stream();
-    void* in = ws_get(c, "rp_in", kkt_block_bytes(k, es, 1));
-    const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st);
-    void* dl = ws_get(c, "rp_l", es * D);
+    void* in = ws_get(c, "rp_in", kkt_block_bytes(k, es, 1) + es * D);
+    char* dl = nullptr;
+    const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st, lambda, es * D, &dl);
     void* dd = ws_get(c, "rp_dz", es * P);
-    h2d(c, dl, lambda, es * D, st);
+    void* hd = hws_get(c, "rp_hdz", es * P);
     if (dtype == B2P_F64)
       primal_impl<double>(c, 1, k, kv, dl, dd, st);
     else
       primal_impl<float>(c, 1, k, kv, dl, dd, st);
-    d2h(c, dz_out, dd, es * P, st);
+    d2h(c, hd, dd, es * P, st);
     CK(cudaStreamSynchronize(st));
+    std::memcpy(dz_out, hd, es * P);
   });
 }
 

@@ -98,3 +98,37 @@ def test_b200_batched_device_matches_single(orc):
     for i in range(Bn):
         want = orc.reconstruct_primal(kb.system(i), lam[i])
         assert np.abs(got[i] - want).max() / max(1.0, np.abs(want).max()) <= 1e-12
+
+
+def test_sqp_step_null_dz_is_invalid_argument():  # b2p.h b2p_sqp_step (checked before any device work)
+    import ctypes as C
+    from paper_2309_08079_b200 import _abi, _lib
+    L = _lib.load()
+    err = _abi.ErrorC()
+    rc = L.b2p_sqp_step(None, 0, None, 3, 1, None, None, None, None, None, None, C.byref(err))
+    assert rc == 1 and b"null dz" in err.message
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(31, 14, 7), (8, 3, 2), (127, 14, 7)])
+def test_sqp_step_equals_solve_then_reconstruct(orc, shape):
+    """b2p_sqp_step (one upload, fused solve + primal kernel) returns exactly
+    what b2p_solve followed by b2p_reconstruct_primal return, and agrees with
+    the oracle's linear step, warm start included."""
+    import paper_2309_08079_b200.api as api
+    from paper_2309_08079_b200.types import PcgConfig
+    api.require_device()
+    N, n, m = shape
+    kkt = orc.random_kkt(900 + N, N, n, m)
+    cfg = PcgConfig(epsilon=1e-8)
+    lam0 = 0.01 * orc.UniformRng(5).vector(kkt.dual_dim(), -1.0, 1.0)
+    for l0 in (None, lam0):
+        res, dz = api.sqp_step(kkt, cfg=cfg, lambda0=l0)
+        ref = api.solve(kkt, cfg=cfg, lambda0=l0)
+        assert res.report.iterations == ref.report.iterations
+        assert np.array_equal(res.lambda_, ref.lambda_)
+        assert np.array_equal(dz, api.reconstruct_primal(kkt, ref.lambda_))
+        o = orc.solve(kkt, cfg=cfg, lambda0=l0)
+        assert res.report.iterations == o.report.iterations
+        want = orc.reconstruct_primal(kkt, o.lambda_)
+        assert np.abs(dz - want).max() / max(1.0, np.abs(want).max()) <= 1e-9
