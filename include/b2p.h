@@ -263,6 +263,12 @@ int b2p_random_kkt_batch(int family, uint64_t seed0, int batch, int N, int n, in
                          double diag_floor, double coupling, int threads, b2p_kkt_out* out,
                          b2p_error* err);
 
+/* UniformRng(seed): `count` draws lo + (hi - lo) * ((x >> 11) * 2^-53) of
+ * mt19937_64 in order (random_problem.hpp:13-37) — e.g. the seeded rollout
+ * controls of a named-model problem file (problem_io.cpp:208-214). */
+int b2p_uniform_draws(uint64_t seed, int count, double lo, double hi, double* out,
+                      b2p_error* err);
+
 /* ---- memory helpers (for FFI callers without a CUDA runtime) ----------- */
 void* b2p_host_alloc(size_t bytes); /* pinned */
 void b2p_host_free(void* p);

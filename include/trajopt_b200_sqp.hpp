@@ -20,6 +20,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <fstream>
 #include <functional>
 #include <limits>
 #include <memory>
@@ -751,6 +753,81 @@ inline NmpcStats run_nmpc(const NmpcConfig& cfg, const DynamicsModel& model,
     stats.segment_errors.push_back(sum / static_cast<double>(tail));
   }
   return stats;
+}
+
+// --------------------------------------------------------------- NMPC outputs
+// problem_io.hpp:57-62, problem_io.cpp:250-303 — the run-nmpc CSV / JSON files.
+namespace io_detail {
+inline void write_text_file(const std::string& path, const std::string& content) {
+  std::ofstream out(path, std::ios::binary);
+  if (!out) throw std::runtime_error("cannot write file: " + path);
+  out << content;
+}
+/// nlohmann::json's number format: shortest round-trip digits, ".0" on integral values.
+inline std::string json_number(double v) {
+  char buf[64];
+  for (int prec = 1; prec <= 17; ++prec) {
+    std::snprintf(buf, sizeof(buf), "%.*g", prec, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  std::string s(buf);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+  return s;
+}
+}  // namespace io_detail
+
+/// steps.csv: step,time_s,solve_us,sqp_iters,pcg_iters_total,tracking_err
+inline void write_steps_csv(const NmpcStats& stats, const std::string& path) {
+  std::ostringstream out;
+  out << "step,time_s,solve_us,sqp_iters,pcg_iters_total,tracking_err\n";
+  for (const auto& rec : stats.steps) {
+    const double solve_us = stats.deterministic ? 0.0 : rec.solve_us;
+    out << rec.step << ',' << format9(rec.time_s) << ',' << format9(solve_us) << ','
+        << rec.sqp_iters << ',' << rec.pcg_iters_total << ',' << format9(rec.tracking_err) << '\n';
+  }
+  io_detail::write_text_file(path, out.str());
+}
+
+/// cdf.csv: solve_us,cumulative_fraction (sorted ascending, monotone).
+inline void write_cdf_csv(const NmpcStats& stats, const std::string& path) {
+  std::vector<double> times;
+  times.reserve(stats.steps.size());
+  for (const auto& rec : stats.steps) times.push_back(stats.deterministic ? 0.0 : rec.solve_us);
+  std::sort(times.begin(), times.end());
+  std::ostringstream out;
+  out << "solve_us,cumulative_fraction\n";
+  for (size_t i = 0; i < times.size(); ++i)
+    out << format9(times[i]) << ',' << format9(static_cast<double>(i + 1) / times.size()) << '\n';
+  io_detail::write_text_file(path, out.str());
+}
+
+/// summary.json (keys sorted and indented by 2 like nlohmann::json::dump(2)).
+inline void write_nmpc_summary_json(const NmpcStats& stats, const std::string& path) {
+  using io_detail::json_number;
+  const bool det = stats.deterministic;
+  double mean_track = 0.0;
+  for (const auto& rec : stats.steps) mean_track += rec.tracking_err;
+  if (!stats.steps.empty()) mean_track /= static_cast<double>(stats.steps.size());
+  std::ostringstream out;
+  out << "{\n";
+  out << "  \"max_solve_us\": " << json_number(det ? 0.0 : stats.max_solve_us) << ",\n";
+  out << "  \"mean_solve_us\": " << json_number(det ? 0.0 : stats.mean_solve_us) << ",\n";
+  out << "  \"mean_tracking_err\": " << json_number(mean_track) << ",\n";
+  out << "  \"median_solve_us\": " << json_number(det ? 0.0 : stats.median_solve_us) << ",\n";
+  out << "  \"overruns\": " << (det ? 0 : stats.overruns) << ",\n";
+  out << "  \"p95_solve_us\": " << json_number(det ? 0.0 : stats.p95_solve_us) << ",\n";
+  out << "  \"segment_errors\": ";
+  if (stats.segment_errors.empty()) {
+    out << "[]";
+  } else {
+    out << "[\n";
+    for (size_t i = 0; i < stats.segment_errors.size(); ++i)
+      out << "    " << json_number(stats.segment_errors[i])
+          << (i + 1 < stats.segment_errors.size() ? ",\n" : "\n");
+    out << "  ]";
+  }
+  out << ",\n  \"steps\": " << stats.steps.size() << "\n}\n";
+  io_detail::write_text_file(path, out.str());
 }
 
 }  // namespace trajopt_b200

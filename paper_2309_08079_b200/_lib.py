@@ -65,6 +65,7 @@ def load() -> C.CDLL:
         "b2p_random_kkt": ([i32, u64, i32, i32, i32, dbl, dbl, C.POINTER(_abi.KktOutC), E], i32),
         "b2p_random_kkt_batch": ([i32, u64, i32, i32, i32, i32, dbl, dbl, i32,
                                   C.POINTER(_abi.KktOutC), E], i32),
+        "b2p_uniform_draws": ([u64, i32, dbl, dbl, vp, E], i32),
         "b2p_host_alloc": ([C.c_size_t], vp),
         "b2p_host_free": ([vp], None),
     }
@@ -89,5 +90,5 @@ EXPORTED = [
     "b2p_apply_preconditioner", "b2p_pcg_solve", "b2p_solve", "b2p_solve_batched",
     "b2p_solve_batched_device", "b2p_solve_batched_multi", "b2p_reconstruct_primal",
     "b2p_reconstruct_primal_batched_device", "b2p_sqp_step", "b2p_random_kkt",
-    "b2p_random_kkt_batch", "b2p_host_alloc", "b2p_host_free",
+    "b2p_random_kkt_batch", "b2p_uniform_draws", "b2p_host_alloc", "b2p_host_free",
 ]

@@ -1566,6 +1566,15 @@ int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
 }
 
 // ---------------------------------------------------------------- generator
+int b2p_uniform_draws(uint64_t seed, int count, double lo, double hi, double* out,
+                      b2p_error* err) {
+  return guard(err, [&] {
+    if (count < 0 || (count > 0 && !out)) throw invalid("uniform_draws: bad buffer");
+    Rng g(seed);
+    for (int i = 0; i < count; ++i) out[i] = g.u(lo, hi);
+  });
+}
+
 int b2p_random_kkt(int family, uint64_t seed, int N, int n, int m, double fl, double cp,
                    b2p_kkt_out* out, b2p_error* err) {
   return guard(err, [&] {

@@ -6,9 +6,8 @@ Host-side file formats only (no compute): the explicit-model JSON problem
 document, the benchmark CSV row schema, and `solve_qp`, which mirrors
 `cmd_solve_qp` (proj/tools/trajopt_cli.cpp:88-125) on the B200 path
 (build_schur -> build_preconditioner -> pcg_solve_auto through the C-ABI).
-Named dynamics models (model != "explicit") need the reference's model
-library and linearisation, which are outside the hot-path scope: loading one
-raises InputError.
+Named dynamics models (model != "explicit") are linearised around the seeded
+rollout (models.py, problem_io.cpp:194-216) and solved on the same path.
 """
 from __future__ import annotations
 
@@ -147,10 +146,9 @@ def save_problem(pf: ProblemFile, path: str) -> None:  # problem_io.cpp:178-180
         fh.write(problem_to_json(pf))
 
 
-def problem_to_kkt(pf: ProblemFile) -> KKTSystem:  # problem_io.cpp:182-193
+def problem_to_kkt(pf: ProblemFile) -> KKTSystem:  # problem_io.cpp:182-216
     if pf.model != "explicit":
-        raise InputError(f"problem file: model {pf.model} needs the reference's dynamics models "
-                         "(outside the B200 hot-path scope); use model \"explicit\"")
+        return _named_model_kkt(pf)
     n, m, N = pf.n, pf.m, pf.N
     k = KKTSystem.allocate(N, n, m)
     for i, kd in enumerate(pf.knots):
@@ -165,6 +163,30 @@ def problem_to_kkt(pf: ProblemFile) -> KKTSystem:  # problem_io.cpp:182-193
     k.x_s[:] = pf.x_s if pf.x_s is not None and len(pf.x_s) else 0.0
     k.x0[:] = pf.x0 if pf.x0 is not None and len(pf.x0) else 0.0
     return k
+
+
+def _named_model_kkt(pf: ProblemFile) -> KKTSystem:  # problem_io.cpp:194-216
+    """Linearise a named model around the rollout from x_s: zero controls for seed 0,
+    else controls drawn uniform in [-0.1, 0.1] from UniformRng(seed)."""
+    from . import models
+    try:
+        model = models.make_model(pf.model)
+    except ValueError as e:
+        raise InputError(str(e)) from None
+    if model.state_dim() != pf.n or model.control_dim() != pf.m:
+        raise InputError(f"problem file: model {pf.model} has dims n={model.state_dim()} "
+                         f"m={model.control_dim()}, file says n={pf.n} m={pf.m}")
+    x_start = pf.x_s if pf.x_s is not None and len(pf.x_s) else np.zeros(pf.n)
+    goal = pf.goal if pf.goal is not None and len(pf.goal) else np.zeros(pf.n)
+    cost = models.quadratic_tracking_cost(pf.wx * np.eye(pf.n), pf.wu * np.eye(pf.m),
+                                          pf.wn * np.eye(pf.n), goal)
+    if pf.seed != 0:
+        u = models.uniform_draws(pf.seed, pf.N * pf.m, -0.1, 0.1).reshape(pf.N, pf.m)
+        controls = [u[k] for k in range(pf.N)]
+    else:
+        controls = [np.zeros(pf.m) for _ in range(pf.N)]
+    traj = models.rollout(model, x_start, controls, pf.h)
+    return models.assemble_kkt(traj, model, cost, x_start)
 
 
 def problem_from_kkt(kkt: KKTSystem, seed: int) -> ProblemFile:  # problem_io.cpp:218-229

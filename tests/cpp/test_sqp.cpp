@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <string>
 
 #include "trajopt_b200_sqp.hpp"
@@ -634,6 +635,58 @@ static void test_nmpc() {
   }
 }
 
+// ------------------------------------------------------------------ test_io.cpp:98-140
+static std::vector<std::string> read_lines(const std::string& path) {
+  std::ifstream in(path);
+  std::vector<std::string> out;
+  std::string line;
+  while (std::getline(in, line)) out.push_back(line);
+  return out;
+}
+static void test_nmpc_writers() {
+  NmpcStats stats;
+  stats.deterministic = false;
+  for (int i = 0; i < 5; ++i) {
+    NmpcStepRecord rec;
+    rec.step = i;
+    rec.time_s = 0.01 * i;
+    rec.solve_us = 100.0 - 10.0 * i;  // unsorted on purpose
+    rec.sqp_iters = 2;
+    rec.pcg_iters_total = 6;
+    rec.tracking_err = 0.1;
+    stats.steps.push_back(rec);
+  }
+  stats.segment_errors = {0.25, 1e-3};
+  const std::string steps_path = "/tmp/b2p_test_steps.csv", cdf_path = "/tmp/b2p_test_cdf.csv",
+                    json_path = "/tmp/b2p_test_summary.json";
+  write_steps_csv(stats, steps_path);
+  write_cdf_csv(stats, cdf_path);
+  write_nmpc_summary_json(stats, json_path);
+  const auto sl = read_lines(steps_path);
+  CHECK(sl.size() == 6 && sl[0] == "step,time_s,solve_us,sqp_iters,pcg_iters_total,tracking_err");
+  CHECK(sl[2] == "1,0.01,90,2,6,0.1");
+  const auto cl = read_lines(cdf_path);
+  CHECK(cl.size() == 6 && cl[0] == "solve_us,cumulative_fraction");
+  double prev_t = -1.0, prev_f = 0.0;
+  for (size_t i = 1; i < cl.size(); ++i) {
+    const auto comma = cl[i].find(',');
+    const double t = std::stod(cl[i].substr(0, comma)), f = std::stod(cl[i].substr(comma + 1));
+    CHECK(t >= prev_t && f > prev_f);
+    prev_t = t;
+    prev_f = f;
+  }
+  CHECK(std::abs(prev_f - 1.0) < 1e-12);
+  const auto jl = read_lines(json_path);
+  CHECK(jl.size() == 13 && jl[0] == "{" && jl[1] == "  \"max_solve_us\": 0.0," && jl[3] == "  \"mean_tracking_err\": 0.1," &&
+        jl[8] == "    0.25," && jl[9] == "    0.001" && jl[11] == "  \"steps\": 5");
+  stats.deterministic = true;
+  write_steps_csv(stats, steps_path);
+  CHECK(read_lines(steps_path)[1] == "0,0,0,2,6,0.1");
+  std::remove(steps_path.c_str());
+  std::remove(cdf_path.c_str());
+  std::remove(json_path.c_str());
+}
+
 // ------------------------------------------------------------------ GPU vs oracle parity
 // Same scenario on both linear steps: every SQP iteration must take the same
 // PCG iteration count and the same line-search step, with merits and final
@@ -774,6 +827,7 @@ int main(int argc, char** argv) {
   test_merit_and_line_search();
   test_sqp_solve();
   test_nmpc();
+  test_nmpc_writers();
   if (gpu) {
     test_parity();
     time_linear_step();
