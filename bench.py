@@ -361,7 +361,7 @@ def run_b200(a, world, rank, local):
                            "host copies excluded; median of 20 after 5 warm-up solves"}
         cases = {"c1": (1, 31, 14, 7, np.float64, 1e-8), "c2": (2, 127, 14, 7, np.float64, 1e-8),
                  "c3": (3, 255, 12, 4, np.float32, 1e-4), "c5": (5, 511, 28, 14, np.float64, 1e-8)}
-        names = {0: "split", 1: "one-CTA fused", 2: "fused cluster", 3: "fused grid"}
+        names = {0: "split", 1: "one-CTA fused", 2: "fused cluster", 3: "fused grid", 4: "fused small"}
         for name, (seed, Nk, nk, mk, dt, eps) in cases.items():
             kk = api.random_kkt(seed, Nk, nk, mk)
             lat = []

@@ -132,8 +132,10 @@ int b2p_ctx_set_stream(b2p_ctx* ctx, void* stream);
 void* b2p_ctx_stream(b2p_ctx* ctx);
 /* Number of kernels this context launched since creation (evidence counter). */
 long long b2p_ctx_kernel_launches(b2p_ctx* ctx);
-/* Which device path the most recent fused solve took: 1 = the persistent
- * one-CTA-per-system K1+K3 kernel, 0 = split K1 formation + K3 PCG. */
+/* Which device path the most recent fused solve took: 0 = split K1 formation
+ * + K3 PCG, 1 = the persistent one-CTA-per-system kernel (n14/m7 fp64),
+ * 2 = the cluster kernel, 3 = the cooperative grid kernel, 4 = the small-block
+ * one-CTA kernel (n, m <= 8 fp64). */
 int b2p_ctx_last_path(b2p_ctx* ctx);
 /* Debug (B2P_PHASE_TIMING=1): per-system %globaltimer stamps of the last
  * one-CTA fused solve, [n][8] = start, F1 end, F2 end, staging end, end (ns).

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libb2p.so")
-SOURCES = ["b2p_api.cu", "schur_kernels.cu", "pcg_kernels.cu", "fused_kernels.cu", "fc_kernels.cu", "fg_kernels.cu", "primal_kernels.cu"]
+SOURCES = ["b2p_api.cu", "schur_kernels.cu", "pcg_kernels.cu", "fused_kernels.cu", "fc_kernels.cu", "fg_kernels.cu", "primal_kernels.cu", "small_kernels.cu"]
 HEADERS = ["common.cuh", "kernels.h", "warp_dense.cuh", "hw_dense.cuh", "wp_dense.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

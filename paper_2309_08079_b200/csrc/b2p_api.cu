@@ -645,6 +645,55 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     if (time_it) CK(cudaEventRecord(c->ev1, st));
     return;
   }
+  if (!drift && env_int("B2P_FUSED", 1) && env_int("B2P_SMALL", 1) &&
+      small_supported<T>(K, n, k->m, kind)) {
+    // small blocks (n, m <= 8): one CTA per system, all in shared memory
+    // persistent CTAs, no inter-CTA sync: CTAs beyond the resident ones just queue
+    const int grid = std::max(1, std::min(B, c->sm_count * 2));
+    FusedParams<T> f{};
+    f.B = B;
+    f.K = K;
+    f.kind = kind;
+    f.Q = static_cast<const T*>(kv.Q);
+    f.q = static_cast<const T*>(kv.q);
+    f.R = static_cast<const T*>(kv.R);
+    f.r = static_cast<const T*>(kv.r);
+    f.A = static_cast<const T*>(kv.A);
+    f.Bm = static_cast<const T*>(kv.B);
+    f.e = static_cast<const T*>(kv.e);
+    f.x_s = static_cast<const T*>(kv.x_s);
+    f.x0 = static_cast<const T*>(kv.x0);
+    f.lambda0 = static_cast<const T*>(lambda0);
+    f.lambda_out = static_cast<T*>(lambda_out);
+    f.errkey = errkey;
+    f.out = outs_dev;
+    f.trace = trace_dev;
+    f.trace_cap = trace_cap;
+    f.epsilon = cfg ? cfg->epsilon : 1e-4;
+    const int mi = cfg ? cfg->max_iter : 0;
+    f.max_iter = mi > 0 ? mi : static_cast<int>(D);
+    if (time_it) {
+      if (!c->accounting) c->pool_used = 0;
+      if (c->pool_used + 3 > c->pool.size())
+        for (int q = 0; q < 3; ++q) {
+          cudaEvent_t e;
+          CK(cudaEventCreate(&e));
+          c->pool.push_back(e);
+        }
+      c->ev0 = c->pool[c->pool_used];
+      c->ev2 = c->pool[c->pool_used + 1];
+      c->ev1 = c->pool[c->pool_used + 2];
+      c->pool_used += 3;
+      CK(cudaEventRecord(c->ev0, st));
+      CK(cudaEventRecord(c->ev2, st));
+    }
+    CK(launch_small<T>(f, n, k->m, grid, st));
+    c->launches++;
+    c->last_path = 4;
+    c->phases = time_it;
+    if (time_it) CK(cudaEventRecord(c->ev1, st));
+    return;
+  }
   c->last_path = 0;
   T* S = static_cast<T*>(ws_get(c, tag + "S", sizeof(T) * B * K * 3 * nn));
   T* gamma = static_cast<T*>(ws_get(c, tag + "gamma", sizeof(T) * B * D));

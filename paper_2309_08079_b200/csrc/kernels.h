@@ -87,6 +87,12 @@ template <class T> bool fused_supported(int K, int n, int m, int kind);
 template <class T> size_t fused_slot_elems(int K, int n, int m);
 template <class T> cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st);
 
+// Fused one-CTA kernel for small blocks (small_kernels.cu): n, m <= 8 padded
+// to powers of two, everything in shared memory (the SQP / NMPC shapes).
+template <class T> bool small_supported(int K, int n, int m, int kind);
+template <class T>
+cudaError_t launch_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st);
+
 // Fused cluster kernel (fc_kernels.cu): one thread-block cluster of G CTAs per
 // system. fc_pick_g returns the cluster size for a shape (0 = unsupported).
 template <class T> int fc_pick_g(int K, int n, int m, int kind, int B);

@@ -45,7 +45,8 @@ def timed(kkt, kind, eps, dtype=np.float64, env=None):
         orc_res = orc.solve(kkt, kind, 1, cfg, dtype=dtype)
         cpu_us = (time.perf_counter() - t0) * 1e6
         ctx = api.context()
-        path = {0: "split K1+K3", 1: "fused one-CTA", 2: "fused cluster", 3: "fused grid"}[ctx.last_path()]
+        path = {0: "split K1+K3", 1: "fused one-CTA", 2: "fused cluster", 3: "fused grid",
+                4: "fused small"}[ctx.last_path()]
         k1_ms, k3_ms = ctx.last_phase_ms()
         return {"us_median": statistics.median(ts), "us_min": min(ts),
                 "iterations": res.report.iterations,
