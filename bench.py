@@ -375,6 +375,22 @@ def run_b200(a, world, rank, local):
                              "dtype": np.dtype(dt).name, "epsilon": eps,
                              "kernel": names.get(api.context().last_path(), "?")}
         latency["c1_us_median"] = latency["c1"]["us_median"]
+        # The SQP linear step of the reference's NMPC caller (sqp.cpp:171-176) at the
+        # test-suite shape (double integrator, N = 32): one b2p_sqp_step call from host
+        # buffers — fused solve + reconstruct_primal on one staged upload — wall clock
+        # around the call (host packing, copies, launch and sync included).
+        kq = api.random_kkt(11, 32, 2, 1)
+        wall = []
+        rq = None
+        for i in range(45):
+            t0 = time.perf_counter()
+            rq, _dz = api.sqp_step(kq, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
+            if i >= 5:
+                wall.append((time.perf_counter() - t0) * 1e6)
+        latency["sqp_step_n2"] = {"us_median_host_wall": statistics.median(wall),
+                                  "us_device": rq.report.wall_time * 1e6,
+                                  "iterations": rq.report.iterations, "knots": 33, "nx": 2,
+                                  "nu": 1, "kernel": names.get(api.context().last_path(), "?")}
         # c1 through a CUDA graph ("c1 is also reported via a CUDA Graph to
         # show the launch floor"): device-resident inputs, the solve captured once and
         # replayed back to back; per-replay time = launch floor + kernel

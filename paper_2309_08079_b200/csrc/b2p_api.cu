@@ -687,6 +687,11 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       CK(cudaEventRecord(c->ev0, st));
       CK(cudaEventRecord(c->ev2, st));
     }
+    f.timing = env_int("B2P_PHASE_TIMING", 0)
+                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
+                   : nullptr;
+    c->timing = f.timing;
+    c->timing_n = f.timing ? B : 0;
     CK(launch_small<T>(f, n, k->m, grid, st));
     c->launches++;
     c->last_path = 4;

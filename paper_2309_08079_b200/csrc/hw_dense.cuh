@@ -274,16 +274,17 @@ __device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd
 // independent matrices at once (lanes 0-7 and 8-15). l = lane & 7; every lane
 // of the warp must call it (full-warp mask, width-8 shuffles); Lr / LiT / rd
 // are the calling group's own tiles.
-template <class T, int N>
+// W: group width (lanes per matrix, N <= W <= 8; W = 2 / 4 packs 16 / 8 groups per warp).
+template <class T, int N, int W = 8>
 __device__ __forceinline__ int g8_spd_inverse(T (&a)[N], T* Lr, T* LiT, T* rd, int l, T (&x)[N]) {
-  static_assert(N <= 8, "8-lane groups");
+  static_assert(N <= W && W <= 8, "N <= W <= 8 lanes per group");
   int fail = -1;
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     T s = a[k];
 #pragma unroll
     for (int q = 0; q < k; ++q) s -= a[q] * Lr[k * N + q];
-    T piv = __shfl_sync(FULL, s, k, 8);
+    T piv = __shfl_sync(FULL, s, k, W);
     const bool bad = piv <= T(0);  // x <= 0 fails, NaN passes (Eigen LLT)
     fail = (bad && fail < 0) ? k : fail;
     piv = bad ? T(1) : piv;

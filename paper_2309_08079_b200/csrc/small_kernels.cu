@@ -12,10 +12,10 @@
 // D, theta^-1 are identity rows, of L zero), and every row product sums its
 // n real terms first, then exact zeros — the same values as an n-term loop.
 //
-//   F1 (schur.cpp:15-23,49-51): 8-lane group per knot: Q_k^-1, Q_k^-1 q_k,
+//   F1 (schur.cpp:15-23,49-51): one lane group (GW = max(NP, MP, 2) lanes) per knot: Q_k^-1, Q_k^-1 q_k,
 //      R_k^-1, R_k^-1 r_k (Cholesky + triangular inverse in Eigen's LLT order,
 //      g8_spd_inverse, which also flags the first non-PD pivot).
-//   F2 (schur.cpp:53-78): 8-lane group per block row, lane l = row l:
+//   F2 (schur.cpp:53-78): one lane group per block row, lane l = row l:
 //      AQ = A Q_k^-1, L_b = -AQ, BR = B R_k^-1,
 //      theta = sym(AQ A' + BR B' + Q_{k+1}^-1), gamma_b = e_k - zeta,
 //      theta_b^-1; row 0: D = Q_0^-1, theta^-1[0] = sym(Q_0) (the reference's).
@@ -30,30 +30,26 @@ namespace b2p {
 namespace {
 
 constexpr int kSmallThreads = 256;
-constexpr int kGroups = kSmallThreads / 8;
+// lanes per block-row group: the padded block size (>= 2), so n <= 2 packs 128
+// groups per CTA and a K = 33 horizon forms in one trip instead of two
+template <int NP, int MP>
+constexpr int group_width() {
+  return (NP > MP ? NP : MP) < 2 ? 2 : (NP > MP ? NP : MP);
+}
 
 template <int NP, int MP>
 struct SmallLayout {
   static constexpr int NN = NP * NP, MM = MP * MP;
-  // per 8-lane group: Lr, LiT, sym tile, rd (n-sized) + Lr, LiT, rd (m-sized)
+  static constexpr int GW = group_width<NP, MP>(), kGroups = kSmallThreads / GW;
+  // per lane group: Lr, LiT, sym tile, rd (n-sized) + Lr, LiT, rd (m-sized)
   static constexpr int tile = 3 * NN + NP + 2 * MM + MP;
-  // persistent: D, L, theta^-1 [K][NN], gamma [K][NP]
-  __host__ __device__ static size_t persistent(int K) { return size_t(K) * (3 * NN + NP); }
-  // formation scratch (aliased by the PCG vectors afterwards)
-  __host__ __device__ static size_t form(int K) {
-    const int N = K > 1 ? K - 1 : 1;
-    return size_t(K) * (NN + NP) + size_t(N) * (MM + MP) + size_t(kGroups) * tile + staged(K);
-  }
-  // staged knot data, bounded by the padded sizes (n <= NP, m <= MP)
-  __host__ __device__ static size_t staged(int K) {
-    const size_t N = K > 1 ? K - 1 : 0;
-    return size_t(K) * (NN + NP) + N * (MM + MP + NN + NP * MP + NP) + 2 * NP;
-  }
-  __host__ __device__ static size_t pcg(int K) { return size_t(8) * K * NP + 64; }
-  __host__ __device__ static size_t total(int K) {
-    return persistent(K) + (form(K) > pcg(K) ? form(K) : pcg(K));
-  }
 };
+
+__device__ __forceinline__ unsigned long long small_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int TEAM>
 __device__ __forceinline__ void team_sync() {
@@ -282,14 +278,16 @@ __device__ void small_pcg(const FusedParams<T>& p, int sys, int n, int K, const 
 }
 
 template <class T, int NP, int MP>
-__global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p, int n, int m) {
+__global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p, int n, int m,
+                                                               int staged) {
   using L = SmallLayout<NP, MP>;
   constexpr int NN = L::NN, MM = L::MM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
   const int K = p.K, N = K - 1;
   const int tid = threadIdx.x;
-  const int g = tid >> 3, l = tid & 7;
+  constexpr int GW = L::GW, kGroups = L::kGroups;
+  const int g = tid / GW, l = tid % GW;
   const int lr = l < NP ? l : NP - 1;  // clamped row for duplicate lanes
   // persistent
   T* sD = smem;
@@ -315,8 +313,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p,
 
   for (int sys = blockIdx.x; sys < p.B; sys += gridDim.x) {
     __syncthreads();  // previous system done with shared memory
+    unsigned long long* tm = (p.timing && tid == 0) ? p.timing + size_t(sys) * 8 : nullptr;
+    if (tm) tm[0] = small_gtimer();
     // Stage the system's knot data (the b2p_kkt layout, unpadded) in shared
-    // memory with coalesced loads, all issued before any is consumed: the
+    // memory with coalesced cp.async copies, all issued before any is consumed: the
     // formation then reads operands at shared-memory latency instead of one
     // dependent L2/HBM round trip per product.
     const size_t cnt[9] = {size_t(K) * n * n, size_t(K) * n,     size_t(N) * m * m,
@@ -329,15 +329,27 @@ __global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p,
 #pragma unroll 1
       for (int a = 0; a < 9; ++a) {
         const T* src = gsrc[a] + size_t(sys) * cnt[a];
-        for (size_t i = tid; i < cnt[a]; i += kSmallThreads) d[i] = __ldg(src + i);
-        st[a] = d;
-        d += cnt[a];
+        if (staged) {
+          // asynchronous 8-byte copies: every array's loads are in flight at
+          // once (one memory latency for the whole system, not one per array)
+          const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(d));
+          for (size_t i = tid; i < cnt[a]; i += kSmallThreads)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * unsigned(i)),
+                         "l"(src + i)
+                         : "memory");
+          st[a] = d;
+          d += cnt[a];
+        } else {
+          st[a] = src;  // too long a horizon to stage: read through L1/L2
+        }
       }
     }
     const T *Qs = st[0], *qs = st[1], *Rs = st[2], *rs = st[3], *As = st[4], *Bs = st[5],
             *es = st[6], *xs = st[7], *x0 = st[8];
     if (tid == 0) s_err = 0x7fffffff;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
+    if (tm) tm[1] = small_gtimer();
     int fkey = 0x7fffffff;
 
     // ================================================================ F1
@@ -354,7 +366,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p,
       for (int j = 0; j < NP; ++j)
         a[j] = (lr < n && j < n) ? Qs[size_t(k) * n * n + lr * n + j]
                                  : (lr == j ? T(1) : T(0));
-      const int f = hwd::g8_spd_inverse<T, NP>(a, tLr, tLi, trd, l, x);
+      const int f = hwd::g8_spd_inverse<T, NP, GW>(a, tLr, tLi, trd, l, x);
       if (kv && f >= 0) fkey = min(fkey, k == 0 ? 0 : 4 * k + 2);
       if (kv && l < NP) {
         T qq = T(0);
@@ -374,7 +386,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p,
         for (int j = 0; j < MP; ++j)
           ra[j] = (lm < m && j < m) ? Rs[size_t(kr) * m * m + lm * m + j]
                                     : (lm == j ? T(1) : T(0));
-        const int fr = hwd::g8_spd_inverse<T, MP>(ra, tLr2, tLi2, trd2, l, y);
+        const int fr = hwd::g8_spd_inverse<T, MP, GW>(ra, tLr2, tLi2, trd2, l, y);
         if (rv && fr >= 0) fkey = min(fkey, 4 * (kr + 1) + 1);
         if (rv && l < MP) {
           T rr = T(0);
@@ -388,6 +400,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p,
       }
     }
     __syncthreads();
+    if (tm) tm[2] = small_gtimer();
 
     // ================================================================ F2
 #pragma unroll 1
@@ -470,7 +483,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p,
           for (int j = 0; j < NP; ++j) sD[size_t(b) * NN + l * NP + j] = th[j];
         }
         T x[NP];
-        const int f = hwd::g8_spd_inverse<T, NP>(th, tLr, tLi, trd, l, x);
+        const int f = hwd::g8_spd_inverse<T, NP, GW>(th, tLr, tLi, trd, l, x);
         if (store && f >= 0) fkey = min(fkey, 4 * b + 3);
         if (store) {
 #pragma unroll
@@ -494,35 +507,41 @@ __global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p,
     if (tid == 0 && p.errkey) p.errkey[sys] = 0x7f7f7f7f;
 
     // ================================================================ P
+    if (tm) tm[3] = small_gtimer();
     small_pcg<T, NP, kSmallThreads>(p, sys, n, K, sD, sL, sTi, sG, U);
+    if (tm) tm[4] = small_gtimer();
   }
 }
 
 int pad_pow2(int v) { return v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : v <= 8 ? 8 : 0; }
 
-template <int NP, int MP>
-size_t small_bytes(int K) {
-  return sizeof(double) * SmallLayout<NP, MP>::total(K);
-}
-
-size_t small_bytes_rt(int NP, int MP, int K) {
+// Shared memory of one CTA: persistent D, L, theta^-1 [K][NP][NP] + gamma
+// [K][NP], then the formation scratch (Q^-1, Q^-1 q, R^-1, R^-1 r, the
+// per-group inverse tiles and, when `staged`, the system's knot data) aliased
+// by the PCG vectors.
+size_t small_bytes_rt(int NP, int MP, int K, bool staged) {
   const size_t NN = size_t(NP) * NP, MM = size_t(MP) * MP, N = K > 1 ? K - 1 : 0;
+  const int GW = std::max(2, std::max(NP, MP));
   const size_t tile = 3 * NN + NP + 2 * MM + MP;
-  const size_t staged = size_t(K) * (NN + NP) + N * (MM + MP + NN + NP * MP + NP) + 2 * NP;
+  const size_t stg =
+      staged ? size_t(K) * (NN + NP) + N * (MM + MP + NN + NP * MP + NP) + 2 * NP : 0;
   const size_t form_t = size_t(K) * (NN + NP) + std::max<size_t>(N, 1) * (MM + MP) +
-                        size_t(kGroups) * tile + staged;
+                        size_t(kSmallThreads / GW) * tile + stg;
   const size_t pcg = size_t(8) * K * NP + 64;
   return sizeof(double) * (size_t(K) * (3 * NN + NP) + std::max(form_t, pcg));
 }
 
+constexpr size_t kSmallSmemCap = 227 * 1024 - 1024;
+
 template <class T, int NP, int MP>
 cudaError_t go_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
-  const size_t smem = small_bytes<NP, MP>(p.K);
+  const bool staged = small_bytes_rt(NP, MP, p.K, true) <= kSmallSmemCap;
+  const size_t smem = small_bytes_rt(NP, MP, p.K, staged);
   auto kern = k_fused_small<T, NP, MP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<grid, kSmallThreads, smem, st>>>(p, n, m);
+  kern<<<grid, kSmallThreads, smem, st>>>(p, n, m, staged ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -543,7 +562,7 @@ template <class T>
 bool small_supported(int K, int n, int m, int kind) {
   if (sizeof(T) != 8 || kind == kPoly) return false;
   if (n < 1 || n > 8 || m < 1 || m > 8 || K < 1) return false;
-  return small_bytes_rt(pad_pow2(n), pad_pow2(m), K) + 1024 <= 227 * 1024;
+  return small_bytes_rt(pad_pow2(n), pad_pow2(m), K, false) <= kSmallSmemCap;
 }
 
 template <class T>
