@@ -449,9 +449,12 @@ def run_b200(a, world, rank, local):
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    onchip = None
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            tj = json.load(open(tpath))
+            traffic = tj.get(dom)
+            onchip = tj.get("onchip", {}).get(dom)
         except Exception:
             traffic = None
     flops_step = B * alg["f_full"]
@@ -481,7 +484,10 @@ def run_b200(a, world, rank, local):
                               / FP64_PEAK_TFLOPS,
                               "flops_per_step": flops_step,
                               "peak_source": "measured DFMA microbenchmark "
-                                             "(scripts/micro/lat_bench.cu)"}},
+                                             "(scripts/micro/lat_bench.cu)"},
+                     # the roof that binds: the SM's L1 / shared-memory pipe (ncu capture
+                     # of the same kernel; the PCG and formation operands are on-chip)
+                     "onchip": onchip},
         "pcg_iters": {"mean": mean_iters, "min": int(min(iters)), "max": int(max(iters))},
         "latency": latency,
         "reconstruct_primal": primal,
