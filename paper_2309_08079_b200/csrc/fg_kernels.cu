@@ -517,7 +517,11 @@ __global__ void __launch_bounds__(32 * (FgMaxRp<T, NB>::v + 1), 1)
     const T* Lcol = sL + (w + 1) * FL::pNN + lr;  // column l of L_{b+1}
     T* myP = sP + (w + 1) * VS;
 
+    // Warps without a row (the halo-knot warp, short last CTAs) skip the row
+    // products: their operand rows would lie past the arrays, in buffers other
+    // warps are writing (discarded values, but a shared-memory race).
     auto Srow = [&]() -> T {  // ((D p_b + L p_{b-1}) + R p_{b+1}), block_tri.cpp:82-92
+      if (!rowv) return T(0);
       T out = dot_row<T, NB>(Dw, myP);
       if (hasL) out += dot_reg<T, NB>(lrow, myP - VS);
       if (hasR) out += dot_col<T, NB>(Lcol, myP + VS);
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(32 * (FgMaxRp<T, NB>::v + 1), 1)
       if (p.kind == kIdentity) return rv;
       if (act) sU[w * VS + l] = rv;
       __syncwarp();
-      const T tv = dot_reg<T, NB>(ti, sU + w * VS);
+      const T tv = rowv ? dot_reg<T, NB>(ti, sU + w * VS) : T(0);
       if (!stairish) return tv;
       if (act) sT[(w + 1) * VS + l] = tv;
       if (G > 1) {
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(32 * (FgMaxRp<T, NB>::v + 1), 1)
       if (act) sU[w * VS + l] = uv;
       __syncwarp();
       const bool corr = (p.kind == kSymStair) || (b & 1);
-      return corr ? dot_reg<T, NB>(ti, sU + w * VS) : tv;
+      return (corr && rowv) ? dot_reg<T, NB>(ti, sU + w * VS) : tv;
     };
     // publish the boundary rows of r~ (read by the neighbours after the eta reduction)
     auto publish_rt = [&](T rt) {

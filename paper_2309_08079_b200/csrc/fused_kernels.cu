@@ -580,8 +580,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     __syncthreads();
 
     int bc[R];  // clamped block row per owned row
+    int bl[R], bn[R];  // its neighbour rows, clamped into [0, K): the edge rows'
+                       // products are discarded, but must not read the next
+                       // shared-memory array while other threads write it
 #pragma unroll
-    for (int r = 0; r < R; ++r) bc[r] = bb[r] < K ? bb[r] : K - 1;
+    for (int r = 0; r < R; ++r) {
+      bc[r] = bb[r] < K ? bb[r] : K - 1;
+      bl[r] = bc[r] > 0 ? bc[r] - 1 : 0;
+      bn[r] = bc[r] + 1 < K ? bc[r] + 1 : K - 1;
+    }
     // y_r = ((D x_b + L x_{b-1}) + R x_{b+1}) for the R owned rows, R_b = L_{b+1}'
     // (block_tri.cpp:82-92). Out-of-range neighbours are computed on
     // in-bounds shared memory and discarded by the selects.
@@ -594,12 +601,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         tm_ld_row14(colD(r), m);
         sd[r] = dot_rm<NB>(m, x + bc[r] * NB);
         tm_ld_row14(colL(r), m);
-        sl[r] = dot_rm<NB>(m, x + (bc[r] - 1) * NB);
+        sl[r] = dot_rm<NB>(m, x + bl[r] * NB);
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        Mp[r] = sL + static_cast<size_t>(bc[r] + 1) * NN + l;
-        Xp[r] = x + (bc[r] + 1) * NB;
+        Mp[r] = sL + static_cast<size_t>(bn[r]) * NN + l;
+        Xp[r] = x + bn[r] * NB;
       }
       dots_col<T, NB, R>(Mp, Xp, sr);
 #pragma unroll
@@ -651,12 +658,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int r = 0; r < R; ++r) {
           T m[NB];
           tm_ld_row14(colL(r), m);
-          sl[r] = dot_rm<NB>(m, st + (bc[r] - 1) * NB);
+          sl[r] = dot_rm<NB>(m, st + bl[r] * NB);
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          Mp[r] = sL + static_cast<size_t>(bc[r] + 1) * NN + l;
-          Xp[r] = st + (bc[r] + 1) * NB;
+          Mp[r] = sL + static_cast<size_t>(bn[r]) * NN + l;
+          Xp[r] = st + bn[r] * NB;
         }
         dots_col<T, NB, R>(Mp, Xp, sr);
       }

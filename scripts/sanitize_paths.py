@@ -1,0 +1,33 @@
+"""One small solve on every kernel path, for compute-sanitizer (memcheck / racecheck /
+synccheck) runs: python scripts/sanitize_paths.py"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import paper_2309_08079_b200.api as api  # noqa: E402
+from paper_2309_08079_b200.types import PcgConfig, PrecondKind  # noqa: E402
+
+cfg = PcgConfig(epsilon=1e-8)
+cases = [
+    ("one-CTA fused (c1)", {}, (31, 14, 7), np.float64),
+    ("fused grid (c2-like)", {"B2P_FG": "1"}, (63, 14, 7), np.float64),
+    ("fused cluster (c3-like)", {"B2P_FC": "1"}, (63, 12, 4), np.float32),
+    ("small-block", {}, (32, 2, 1), np.float64),
+    ("small-block n4", {}, (40, 4, 2), np.float64),
+    ("split", {"B2P_FUSED": "0"}, (20, 3, 2), np.float64),
+]
+for name, env, (N, n, m), dt in cases:
+    saved = dict(os.environ)
+    os.environ.update(env)
+    kkt = api.random_kkt(7, N, n, m)
+    for kind in (PrecondKind.symmetric_stair, PrecondKind.stair, PrecondKind.block_jacobi):
+        r = api.solve(kkt, kind, 1, cfg, dtype=dt)
+    res, dz = api.sqp_step(kkt, cfg=cfg) if dt == np.float64 else (r, None)
+    print(name, api.context().last_path(), r.report.iterations, flush=True)
+    os.environ.clear()
+    os.environ.update(saved)
+kb = api.random_kkt_batch(9, 3, 31, 14, 7)
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("batched one-CTA", api.context().last_path(), [x.iterations for x in reps])
