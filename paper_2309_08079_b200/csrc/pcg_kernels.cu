@@ -634,6 +634,8 @@ template <class T>
 cudaError_t launch_pcg(const PcgParams<T>& p, cudaStream_t st) {
   if constexpr (sizeof(T) == 8) {
     if (p.nb == 14) return launch_nb<T, 14>(p, st);
+    if (p.nb == 2) return launch_nb<T, 2>(p, st);  // the SQP / NMPC models
+    if (p.nb == 4) return launch_nb<T, 4>(p, st);
   } else {
     if (p.nb == 12) return launch_nb<T, 12>(p, st);
   }
