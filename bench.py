@@ -429,6 +429,34 @@ def run_b200(a, world, rank, local):
                   "what": "b2p_reconstruct_primal_batched_device over the bench batch "
                           "(kkt.cpp:153-181), CUDA events, inputs in HBM"}
 
+    # ---- direct baseline (the reference bench's "dense_baseline"
+    # row, trajopt_cli.cpp:164-173): build_schur + block-Thomas cholesky_solve of the
+    # same device batch, one warp per system; CUDA events; lambda checked against PCG
+    dense = None
+    if rank == 0 and not a.no_latency:
+        D = (N + 1) * n
+        lam_direct = torch.empty((B, D), dtype=torch.float64, device=f"cuda:{local}")
+        status = torch.empty((B,), dtype=torch.int32, device=f"cuda:{local}")
+        api.direct_solve_batched_device(kd, lam_direct.data_ptr(), status.data_ptr(), B, ctx=ctx)
+        torch.cuda.synchronize()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        d0.record(stream)
+        for _ in range(reps):
+            api.direct_solve_batched_device(kd, lam_direct.data_ptr(), status.data_ptr(), B,
+                                            ctx=ctx)
+        d1.record(stream)
+        torch.cuda.synchronize()
+        dms = d0.elapsed_time(d1) / reps
+        scale = torch.clamp(lam_direct.abs().amax(dim=1), min=1.0)
+        rel = ((lam_direct - lam_dev).abs().amax(dim=1) / scale).max().item()
+        dense = {"systems_per_s": B / (dms * 1e-3), "ms_per_batch": dms,
+                 "all_ok": bool((status == -1).all().item()),
+                 "max_rel_diff_vs_pcg": rel,
+                 "what": "b2p_direct_solve_batched_device: build_schur + block-Thomas "
+                         "cholesky_solve (block_tri.cpp:121-159), one warp per system, on the "
+                         "bench batch; the PCG solves stop at eta' < eps, hence the difference"}
+
     # ---- roofline for the dominant kernel
     mean_iters = float(np.mean(iters))
     alg = algorithmic(N, n, m, mean_iters)
@@ -491,6 +519,7 @@ def run_b200(a, world, rank, local):
         "pcg_iters": {"mean": mean_iters, "min": int(min(iters)), "max": int(max(iters))},
         "latency": latency,
         "reconstruct_primal": primal,
+        "dense_baseline": dense,
         "clocks": clk.summary(),
     }
     if not a.no_cpu and world == 1 and rank == 0:

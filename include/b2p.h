@@ -241,6 +241,15 @@ int b2p_sqp_step(b2p_ctx* ctx, int dtype, const b2p_kkt* kkt, int kind, int orde
                  const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out, void* dz_out,
                  b2p_solve_report* report, double* trace, b2p_error* err);
 
+/* ---- direct baseline (trajopt_cli.cpp:164-173's
+ * "dense_baseline" row): build_schur -> BlockTriMatrix::cholesky_solve(gamma)
+ * (block_tri.cpp:121-159, block Thomas) for a device-resident batch, one warp
+ * per system, launched on the context stream without a host sync.
+ * status_dev[i] = -1 on success, else the first block row whose pivot block
+ * is not positive definite. */
+int b2p_direct_solve_batched_device(b2p_ctx* ctx, int dtype, int batch, const b2p_kkt* kkt_batch_dev,
+                                    void* lambda_dev, int* status_dev, b2p_error* err);
+
 /* Device time (ms) of the most recent solve kernels on this context. */
 int b2p_ctx_last_solve_ms(b2p_ctx* ctx, float* ms);
 /* Per-kernel split of the most recent fused solve: ms[0] = K1 Schur

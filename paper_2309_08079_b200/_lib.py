@@ -61,6 +61,7 @@ def load() -> C.CDLL:
                                      REP, E], i32),
         "b2p_reconstruct_primal": ([vp, i32, KKT, vp, i32, vp, E], i32),
         "b2p_sqp_step": ([vp, i32, KKT, i32, i32, CFG, vp, vp, vp, REP, vp, E], i32),
+        "b2p_direct_solve_batched_device": ([vp, i32, i32, KKT, vp, vp, E], i32),
         "b2p_reconstruct_primal_batched_device": ([vp, i32, i32, KKT, vp, vp, E], i32),
         "b2p_random_kkt": ([i32, u64, i32, i32, i32, dbl, dbl, C.POINTER(_abi.KktOutC), E], i32),
         "b2p_random_kkt_batch": ([i32, u64, i32, i32, i32, i32, dbl, dbl, i32,
@@ -89,6 +90,6 @@ EXPORTED = [
     "b2p_build_schur", "b2p_stair_matrix", "b2p_build_preconditioner",
     "b2p_apply_preconditioner", "b2p_pcg_solve", "b2p_solve", "b2p_solve_batched",
     "b2p_solve_batched_device", "b2p_solve_batched_multi", "b2p_reconstruct_primal",
-    "b2p_reconstruct_primal_batched_device", "b2p_sqp_step", "b2p_random_kkt",
+    "b2p_reconstruct_primal_batched_device", "b2p_sqp_step", "b2p_direct_solve_batched_device", "b2p_random_kkt",
     "b2p_random_kkt_batch", "b2p_uniform_draws", "b2p_host_alloc", "b2p_host_free",
 ]

@@ -418,6 +418,17 @@ def reconstruct_primal_batched_device(kkt_dev: KKTSystem, lambda_ptr: int, dz_pt
                                                         C.byref(err)), err)
 
 
+def direct_solve_batched_device(kkt_dev: KKTSystem, lambda_ptr: int, status_ptr: int, batch: int,
+                                dtype=np.float64, ctx: Context | None = None):
+    """Direct baseline on a device-resident batch: build_schur then the block-Thomas
+    cholesky_solve of S lambda = gamma (block_tri.cpp:121-159); no host sync."""
+    ctx = ctx or context()
+    kc = kkt_dev.to_c(ptr=lambda t: t.data_ptr())
+    err = _abi.ErrorC()
+    _check(load().b2p_direct_solve_batched_device(ctx.handle, _dt(dtype), batch, C.byref(kc),
+                                                  lambda_ptr, status_ptr, C.byref(err)), err)
+
+
 def solve_batched_multi(devices, kkt_batch: KKTSystem, kind=PrecondKind.symmetric_stair,
                         order: int = 1, cfg: PcgConfig | None = None, dtype=np.float64):
     """K4: contiguous batch-index shards, one host thread + context per device."""

@@ -1028,10 +1028,10 @@ int b2p_blocktri_cholesky_solve(b2p_ctx* c, int dtype, int K, int nb, const void
     h2d(c, dM, M, es * K * 3 * nn, st);
     h2d(c, db, rhs, es * D, st);
     if (dtype == B2P_F64)
-      CK(launch_block_cholesky<double>(K, nb, (double*)dM, (double*)db, (double*)dx, (double*)dF,
+      CK(launch_block_cholesky<double>(1, K, nb, (double*)dM, (double*)db, (double*)dx, (double*)dF,
                                        (double*)dy, dst, st));
     else
-      CK(launch_block_cholesky<float>(K, nb, (float*)dM, (float*)db, (float*)dx, (float*)dF,
+      CK(launch_block_cholesky<float>(1, K, nb, (float*)dM, (float*)db, (float*)dx, (float*)dF,
                                       (float*)dy, dst, st));
     c->launches++;
     int status = 0;
@@ -1432,6 +1432,37 @@ int b2p_reconstruct_primal(b2p_ctx* c, int dtype, const b2p_kkt* k, const void* 
     d2h(c, hd, dd, es * P, st);
     CK(cudaStreamSynchronize(st));
     std::memcpy(dz_out, hd, es * P);
+  });
+}
+
+int b2p_direct_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd,
+                                    void* lambda_dev, int* status_dev, b2p_error* err) {
+  return guard(err, [&] {
+    check_dtype(dtype);
+    check_kkt(kd);
+    check_ctx(c);
+    if (batch < 1) throw invalid("direct_solve: batch must be >= 1");
+    if (!lambda_dev || !status_dev) throw invalid("direct_solve: null buffer");
+    const KktDev kv = dev_view(kd);
+    const int K = kd->N + 1, n = kd->n;
+    const size_t es = esize(dtype), nn = size_t(n) * n, D = size_t(K) * n, B = batch;
+    cudaStream_t st = c->stream();
+    void* S = ws_get(c, "ds_S", es * B * K * 3 * nn);
+    void* g = ws_get(c, "ds_g", es * B * D);
+    void* ti = ws_get(c, "ds_t", es * B * K * nn);
+    void* F = ws_get(c, "ds_F", es * B * K * nn);
+    void* y = ws_get(c, "ds_y", es * B * D);
+    int* ek = static_cast<int*>(ws_get(c, "ds_ek", sizeof(int) * B));
+    if (dtype == B2P_F64) {
+      launch_form<double>(c, kd, kv, batch, (double*)S, (double*)g, (double*)ti, ek, st);
+      CK(launch_block_cholesky<double>(batch, K, n, (double*)S, (double*)g, (double*)lambda_dev,
+                                       (double*)F, (double*)y, status_dev, st));
+    } else {
+      launch_form<float>(c, kd, kv, batch, (float*)S, (float*)g, (float*)ti, ek, st);
+      CK(launch_block_cholesky<float>(batch, K, n, (float*)S, (float*)g, (float*)lambda_dev,
+                                      (float*)F, (float*)y, status_dev, st));
+    }
+    c->launches++;
   });
 }
 

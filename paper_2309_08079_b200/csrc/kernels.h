@@ -141,8 +141,8 @@ cudaError_t launch_stair_matrix(int K, int nb, const T* S, T* psi, cudaStream_t 
 template <class T>
 cudaError_t launch_blocktri_check(int K, int nb, const T* M, double* out2, cudaStream_t st);
 template <class T>
-cudaError_t launch_block_cholesky(int K, int nb, const T* M, const T* rhs, T* x, T* factors, T* y,
-                                  int* status, cudaStream_t st);
+cudaError_t launch_block_cholesky(int B, int K, int nb, const T* M, const T* rhs, T* x, T* factors,
+                                  T* y, int* status, cudaStream_t st);
 template <class T> cudaError_t launch_pcg(const PcgParams<T>& p, cudaStream_t st);
 
 }  // namespace b2p

@@ -352,7 +352,8 @@ __global__ void k_blocktri_check(int K, int nb, const T* __restrict__ M, double*
 }
 
 // BlockTriMatrix::cholesky_solve (block_tri.cpp:121-159): block Thomas, one
-// warp per system (the recurrence is sequential in the block row).
+// warp per system (the recurrence is sequential in the block row); blockIdx.x
+// is the system of a batch laid out [B][...] contiguously.
 template <class T>
 __global__ void k_block_cholesky(int K, int nb, const T* __restrict__ M, const T* __restrict__ rhs,
                                  T* __restrict__ x, T* __restrict__ factors, T* __restrict__ y,
@@ -362,6 +363,15 @@ __global__ void k_block_cholesky(int K, int nb, const T* __restrict__ M, const T
   if (threadIdx.x >= 32) return;
   const int n = nb, ld = tile_ld(nb);
   const size_t nn = static_cast<size_t>(n) * n;
+  {
+    const size_t sys = blockIdx.x, D = static_cast<size_t>(K) * n;
+    M += sys * K * 3 * nn;
+    rhs += sys * D;
+    x += sys * D;
+    y += sys * D;
+    factors += sys * K * nn;
+    status += sys;
+  }
   T* base = reinterpret_cast<T*>(smem_raw);
   Tile<T> tF{base, ld}, tL{base + n * ld, ld}, tX{base + 2 * n * ld, ld}, tW{base + 3 * n * ld, ld};
   T* v = base + 4 * n * ld;
@@ -498,14 +508,14 @@ cudaError_t launch_blocktri_check(int K, int nb, const T* M, double* out2, cudaS
 }
 
 template <class T>
-cudaError_t launch_block_cholesky(int K, int nb, const T* M, const T* rhs, T* x, T* factors, T* y,
-                                  int* status, cudaStream_t st) {
+cudaError_t launch_block_cholesky(int B, int K, int nb, const T* M, const T* rhs, T* x, T* factors,
+                                  T* y, int* status, cudaStream_t st) {
   const int ld = tile_ld(nb);
   const size_t smem = sizeof(T) * (4 * nb * ld + 64);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_block_cholesky<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-  k_block_cholesky<T><<<1, 32, smem, st>>>(K, nb, M, rhs, x, factors, y, status);
+  k_block_cholesky<T><<<B, 32, smem, st>>>(K, nb, M, rhs, x, factors, y, status);
   return cudaGetLastError();
 }
 
@@ -516,7 +526,8 @@ cudaError_t launch_block_cholesky(int K, int nb, const T* M, const T* rhs, T* x,
                                                  const T*, T*, cudaStream_t);                  \
   template cudaError_t launch_stair_matrix<T>(int, int, const T*, T*, cudaStream_t);           \
   template cudaError_t launch_blocktri_check<T>(int, int, const T*, double*, cudaStream_t);    \
-  template cudaError_t launch_block_cholesky<T>(int, int, const T*, const T*, T*, T*, T*, int*, \
+  template cudaError_t launch_block_cholesky<T>(int, int, int, const T*, const T*, T*, T*, T*,  \
+                                                int*,                                         \
                                                 cudaStream_t);
 B2P_INST(double)
 B2P_INST(float)

@@ -100,3 +100,30 @@ def test_property_matvec_matches_dense_across_sizes(B, orc):  # :115-127
             seed += 1
             x = orc.UniformRng(seed * 31 + 1).vector(M.dim(), -1.0, 1.0)
             assert rel_inf_error(B.matvec(M, x), M.to_dense() @ x) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_direct_solve_batched_device_matches_cholesky_and_pcg(orc):
+    """b2p_direct_solve_batched_device (the bench's dense_baseline row): per system
+    the same lambda as the single-system cholesky_solve and a tight PCG solve."""
+    import torch
+    import paper_2309_08079_b200.api as api
+    from paper_2309_08079_b200.types import KKTSystem, PcgConfig
+    api.require_device()
+    for (Bn, N, n, m) in [(5, 31, 14, 7), (3, 20, 4, 2)]:
+        kb = api.random_kkt_batch(321 + n, Bn, N, n, m)
+        dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in kb.arrays()]
+        kd = KKTSystem(N, n, m, *dev)
+        D = (N + 1) * n
+        lam = torch.empty((Bn, D), dtype=torch.float64, device="cuda")
+        st = torch.empty((Bn,), dtype=torch.int32, device="cuda")
+        api.direct_solve_batched_device(kd, lam.data_ptr(), st.data_ptr(), Bn)
+        torch.cuda.synchronize()
+        assert (st.cpu().numpy() == -1).all()
+        got = lam.cpu().numpy()
+        for i in range(Bn):
+            sch = orc.build_schur(kb.system(i))
+            want = orc.cholesky_solve(sch.S, sch.gamma)
+            assert np.abs(got[i] - want).max() / max(1.0, np.abs(want).max()) <= 1e-10
+            tight = orc.solve(kb.system(i), cfg=PcgConfig(epsilon=1e-20, max_iter=2000))
+            assert np.abs(got[i] - tight.lambda_).max() / max(1.0, np.abs(want).max()) <= 1e-6
