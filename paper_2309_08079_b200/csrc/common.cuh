@@ -4,6 +4,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace b2p {
 
 // Per-system outcome record written by the kernels and turned into a
@@ -47,5 +52,31 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 __device__ __forceinline__ bool is_finite(double v) { return isfinite(v); }
 __device__ __forceinline__ bool is_finite(float v) { return isfinite(v); }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a host call on every
+// launch otherwise: set it once per (kernel, device) and size high-water mark.
+// The attribute is idempotent, so a race between threads only repeats a call.
+template <class F>
+inline cudaError_t ensure_max_smem(F* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(bytes));
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& v = done[key];
+    v = std::max(v, bytes);
+  }
+  return e;
+}
 
 }  // namespace b2p

@@ -540,8 +540,7 @@ template <class T>
 cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStream_t st) {
   const int rp = (p.K + G - 1) / G;
   auto go = [&](auto kern, size_t smem) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = ensure_max_smem(kern, smem);
     if (e != cudaSuccess) return e;
     if (G > 8) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -728,8 +728,7 @@ template <class T>
 cudaError_t launch_fg(const FusedParams<T>& p, const FgSync<T>& sy, int rp, cudaStream_t st) {
   const int G = (p.K + rp - 1) / rp;
   auto go = [&](auto kern, size_t smem) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = ensure_max_smem(kern, smem);
     if (e != cudaSuccess) return e;
     FusedParams<T> pp = p;
     FgSync<T> ss = sy;

@@ -827,14 +827,12 @@ cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st) {
     const size_t smem = fused_smem_bytes<T, 14, 7>(p.K);
     if (p.K <= kHalfWarps) {
       auto kern = k_fused_cta<T, 14, 7, 1>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem));
+      cudaError_t e = ensure_max_smem(kern, smem);
       if (e != cudaSuccess) return e;
       kern<<<grid, kThreads, smem, st>>>(p);
     } else {
       auto kern = k_fused_cta<T, 14, 7, 2>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(smem));
+      cudaError_t e = ensure_max_smem(kern, smem);
       if (e != cudaSuccess) return e;
       kern<<<grid, kThreads, smem, st>>>(p);
     }

@@ -582,8 +582,7 @@ template <class T, int MODE, int SYNC, int NBC>
 cudaError_t launch_mode(const PcgParams<T>& p, cudaStream_t st) {
   const size_t smem = pcg_smem_bytes(p);
   auto kern = k_pcg<T, MODE, SYNC, NBC>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_max_smem(kern, smem);
   if (e != cudaSuccess) return e;
   if constexpr (SYNC == kSyncCta) {
     kern<<<p.B, p.nthreads, smem, st>>>(p);

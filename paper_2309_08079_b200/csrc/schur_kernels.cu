@@ -463,8 +463,7 @@ cudaError_t launch_build_schur(const FormParams<T>& p, cudaStream_t st) {
   int wpc = static_cast<int>(std::min<size_t>(8, std::max<size_t>(1, (96 * 1024) / per_warp)));
   const size_t smem = per_warp * wpc;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_build_schur<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    ensure_max_smem(k_build_schur<T>, smem);
   const long long warps = static_cast<long long>(p.B) * (p.N + 1);
   const long long grid = (warps + wpc - 1) / wpc;
   k_build_schur<T><<<static_cast<unsigned>(grid), 32 * wpc, smem, st>>>(p);
@@ -478,8 +477,7 @@ cudaError_t launch_build_precond(const PrecondParams<T>& p, cudaStream_t st) {
   const int wpc = 4;
   const size_t smem = per_warp * wpc;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_build_precond<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    ensure_max_smem(k_build_precond<T>, smem);
   const long long warps = static_cast<long long>(p.B) * p.K;
   k_build_precond<T><<<static_cast<unsigned>((warps + wpc - 1) / wpc), 32 * wpc, smem, st>>>(p);
   return cudaGetLastError();
@@ -513,8 +511,7 @@ cudaError_t launch_block_cholesky(int B, int K, int nb, const T* M, const T* rhs
   const int ld = tile_ld(nb);
   const size_t smem = sizeof(T) * (4 * nb * ld + 64);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_block_cholesky<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    ensure_max_smem(k_block_cholesky<T>, smem);
   k_block_cholesky<T><<<B, 32, smem, st>>>(K, nb, M, rhs, x, factors, y, status);
   return cudaGetLastError();
 }

@@ -538,8 +538,7 @@ cudaError_t go_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream
   const bool staged = small_bytes_rt(NP, MP, p.K, true) <= kSmallSmemCap;
   const size_t smem = small_bytes_rt(NP, MP, p.K, staged);
   auto kern = k_fused_small<T, NP, MP>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_max_smem(kern, smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, kSmallThreads, smem, st>>>(p, n, m, staged ? 1 : 0);
   return cudaGetLastError();
