@@ -255,6 +255,36 @@ def c1_graph_latency(api, torch, local, reps=200):
             "matches_eager": ok}
 
 
+def nmpc_batch_throughput(api, torch, local, B=4096, N=32, n=2, m=1, reps=5):
+    """Many independent NMPC-shape systems (double-integrator / pendulum size, the
+    SQP callers' shape) through the small-block kernel, device-resident, CUDA events."""
+    from paper_2309_08079_b200.types import KKTSystem
+    kb = api.random_kkt_batch(77, B, N, n, m)
+    dev = [torch.from_numpy(np.ascontiguousarray(x)).to(f"cuda:{local}") for x in kb.arrays()]
+    kd = KKTSystem(N, n, m, *dev)
+    lam = torch.empty((B, (N + 1) * n), dtype=torch.float64, device=f"cuda:{local}")
+    ctx = api.Context(local)
+    s = torch.cuda.Stream(device=local)
+    ctx.set_stream(s.cuda_stream)
+    cfg = PcgConfig(epsilon=1e-8)
+    with torch.cuda.stream(s):
+        reports = api.solve_batched_device(kd, lam.data_ptr(), B, PrecondKind.symmetric_stair, 1,
+                                           cfg, ctx=ctx, want_reports=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            api.solve_batched_device(kd, lam.data_ptr(), B, PrecondKind.symmetric_stair, 1, cfg,
+                                     ctx=ctx)
+        e1.record(s)
+        s.synchronize()
+    path = ctx.last_path()
+    ctx.close()
+    ms = e0.elapsed_time(e1) / reps
+    return {"systems_per_s": B / (ms * 1e-3), "ms_per_batch": ms, "batch": B, "knots": N + 1,
+            "nx": n, "nu": m, "kernel": {4: "fused small"}.get(path, str(path)),
+            "iters_mean": float(np.mean([r.iterations for r in reports]))}
+
+
 def run_b200(a, world, rank, local):
     import torch
     import paper_2309_08079_b200.api as api
@@ -398,6 +428,10 @@ def run_b200(a, world, rank, local):
             latency["c1_graph"] = c1_graph_latency(api, torch, local)
         except Exception as exc:  # report, do not fail the bench line
             latency["c1_graph"] = {"error": str(exc)[:200]}
+        try:
+            latency["nmpc_batch_n2"] = nmpc_batch_throughput(api, torch, local)
+        except Exception as exc:
+            latency["nmpc_batch_n2"] = {"error": str(exc)[:200]}
 
     # ---- reconstruct_primal on the same batch: dz from the
     # solved lambda, device-resident; HBM-bound (reads the KKT blocks + lambda,

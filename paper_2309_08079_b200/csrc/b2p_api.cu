@@ -648,8 +648,8 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   if (!drift && env_int("B2P_FUSED", 1) && env_int("B2P_SMALL", 1) &&
       small_supported<T>(K, n, k->m, kind)) {
     // small blocks (n, m <= 8): one CTA per system, all in shared memory
-    // persistent CTAs, no inter-CTA sync: CTAs beyond the resident ones just queue
-    const int grid = std::max(1, std::min(B, c->sm_count * 2));
+    // persistent CTAs, as many as fit co-resident (launch_small scales the SM count)
+    const int grid = c->sm_count;
     FusedParams<T> f{};
     f.B = B;
     f.K = K;

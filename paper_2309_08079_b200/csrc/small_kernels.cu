@@ -540,6 +540,11 @@ cudaError_t go_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream
   auto kern = k_fused_small<T, NP, MP>;
   cudaError_t e = ensure_max_smem(kern, smem);
   if (e != cudaSuccess) return e;
+  // persistent CTAs: as many as fit co-resident (`grid` = SM count on entry)
+  int per_sm = 1;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallThreads, smem);
+  if (e != cudaSuccess) return e;
+  grid = std::max(1, std::min(p.B, grid * std::max(1, per_sm)));
   kern<<<grid, kSmallThreads, smem, st>>>(p, n, m, staged ? 1 : 0);
   return cudaGetLastError();
 }
