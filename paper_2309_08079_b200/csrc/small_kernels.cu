@@ -277,8 +277,12 @@ __device__ void small_pcg(const FusedParams<T>& p, int sys, int n, int K, const 
   }
 }
 
-template <class T, int NP, int MP>
-__global__ void __launch_bounds__(kSmallThreads) k_fused_small(FusedParams<T> p, int n, int m,
+// BATCH = true: the throughput build for batches (registers capped so 4 / 3 CTAs
+// fit an SM at n <= 2 / 4: 11.6 -> 15.6 M systems/s at n = 2); BATCH = false:
+// the latency build for single solves (uncapped registers: 30.6 vs 34 us).
+template <class T, int NP, int MP, bool BATCH>
+__global__ void __launch_bounds__(kSmallThreads, (!BATCH ? 1 : (NP <= 2 ? 4 : (NP <= 4 ? 3 : 1))))
+    k_fused_small(FusedParams<T> p, int n, int m,
                                                                int staged) {
   using L = SmallLayout<NP, MP>;
   constexpr int NN = L::NN, MM = L::MM;
@@ -537,7 +541,7 @@ template <class T, int NP, int MP>
 cudaError_t go_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
   const bool staged = small_bytes_rt(NP, MP, p.K, true) <= kSmallSmemCap;
   const size_t smem = small_bytes_rt(NP, MP, p.K, staged);
-  auto kern = k_fused_small<T, NP, MP>;
+  auto kern = p.B > 1 ? k_fused_small<T, NP, MP, true> : k_fused_small<T, NP, MP, false>;
   cudaError_t e = ensure_max_smem(kern, smem);
   if (e != cudaSuccess) return e;
   // persistent CTAs: as many as fit co-resident (`grid` = SM count on entry)
