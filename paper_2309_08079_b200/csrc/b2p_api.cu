@@ -392,6 +392,33 @@ void launch_form(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, T* S, T*
   f.errkey = errkey;
   CK(cudaMemsetAsync(errkey, 0x7f, sizeof(int) * B, st));  // 0x7f7f7f7f: see below
   const int K = k->N + 1;
+  if (env_int("B2P_FUSED", 1) && env_int("B2P_SMALL", 1) &&
+      small_supported<T>(K, k->n, k->m, kSymStair)) {
+    // small blocks: the small-block kernel's formation in formation-only mode
+    FusedParams<T> g{};
+    g.B = B;
+    g.K = K;
+    g.kind = kSymStair;
+    g.Q = f.Q;
+    g.q = f.q;
+    g.R = f.R;
+    g.r = f.r;
+    g.A = f.A;
+    g.Bm = f.Bm;
+    g.e = f.e;
+    g.x_s = f.x_s;
+    g.x0 = f.x0;
+    g.errkey = errkey;
+    g.out = static_cast<SysOut*>(ws_get(c, "form_out", sizeof(SysOut) * B));
+    g.S_out = S;
+    g.gamma_out = gamma;
+    g.theta_out = ti;
+    g.form_only = 1;
+    g.max_iter = 1;
+    CK(launch_small<T>(g, k->n, k->m, c->sm_count, st));
+    c->launches++;
+    return;
+  }
   if (env_int("B2P_FUSED", 1) && fused_supported<T>(K, k->n, k->m, kSymStair)) {
     // the fused kernel's formation phase (shared Q_k^-1, half-warp rows) in
     // formation-only mode writes S / gamma / theta^-1 in the reference layout
@@ -1080,18 +1107,23 @@ int b2p_build_schur(b2p_ctx* c, int dtype, const b2p_kkt* k, void* S, void* gamm
     cudaStream_t st = c->stream();
     void* in = ws_get(c, "bs_in", kkt_block_bytes(k, es, 1));
     const KktDev kv = upload_kkt(c, k, es, 0, 1, in, st);
-    char* dS = static_cast<char*>(ws_get(c, "bs_S", es * K * 3 * nn));
-    char* dg = static_cast<char*>(ws_get(c, "bs_g", es * D));
-    char* dt = static_cast<char*>(ws_get(c, "bs_t", es * K * nn));
-    int* ek = static_cast<int*>(ws_get(c, "bs_ek", sizeof(int)));
+    // outputs in one device block -> one copy back: [key | S | gamma | theta^-1]
+    const size_t bS = es * K * 3 * nn, bg = es * D, bt = es * K * nn;
+    const size_t oS = 256, og = oS + (bS + 255) / 256 * 256, ot = og + (bg + 255) / 256 * 256;
+    const size_t obytes = ot + bt;
+    char* dob = static_cast<char*>(ws_get(c, "bs_ob", obytes));
+    char* hob = static_cast<char*>(hws_get(c, "bs_hob", obytes));
+    char *dS = dob + oS, *dg = dob + og, *dt = dob + ot;
+    int* ek = reinterpret_cast<int*>(dob);
     if (dtype == B2P_F64) launch_form<double>(c, k, kv, 1, (double*)dS, (double*)dg, (double*)dt, ek, st);
     else launch_form<float>(c, k, kv, 1, (float*)dS, (float*)dg, (float*)dt, ek, st);
-    int key = 0;
-    d2h(c, &key, ek, sizeof(int), st);
-    d2h(c, S, dS, es * K * 3 * nn, st);
-    d2h(c, gamma, dg, es * D, st);
-    d2h(c, theta_inv, dt, es * K * nn, st);
+    d2h(c, hob, dob, obytes, st);
     CK(cudaStreamSynchronize(st));
+    int key = 0;
+    std::memcpy(&key, hob, sizeof(int));
+    std::memcpy(S, hob + oS, bS);
+    std::memcpy(gamma, hob + og, bg);
+    std::memcpy(theta_inv, hob + ot, bt);
     if (key < kErrOk) {
       Fail f{B2P_RUNTIME_ERROR, schur_msg(key, nullptr)};
       schur_msg(key, &f.knot);

@@ -510,6 +510,33 @@ __global__ void __launch_bounds__(kSmallThreads, (!BATCH ? 1 : (NP <= 2 ? 4 : (N
     }
     if (tid == 0 && p.errkey) p.errkey[sys] = 0x7f7f7f7f;
 
+    if (p.form_only) {
+      // build_schur only: S in the reference layout [K][left|diag|right][n][n]
+      // (row 0 left and row K-1 right zero, R_b = L_{b+1}'), theta^-1, gamma
+      // — the unpadded leading blocks of the padded shared-memory arrays
+      const int nn = n * n;
+      T* So = p.S_out + size_t(sys) * K * 3 * nn;
+      for (int i = tid; i < K * 3 * nn; i += kSmallThreads) {
+        const int b = i / (3 * nn), rem = i % (3 * nn), slot = rem / nn, e = rem % nn;
+        const int r = e / n, c = e % n;
+        T v = T(0);
+        if (slot == 0)
+          v = b > 0 ? sL[size_t(b) * NN + r * NP + c] : T(0);
+        else if (slot == 1)
+          v = sD[size_t(b) * NN + r * NP + c];
+        else
+          v = b + 1 < K ? sL[size_t(b + 1) * NN + c * NP + r] : T(0);
+        So[i] = v;
+      }
+      for (int i = tid; i < K * nn; i += kSmallThreads) {
+        const int b = i / nn, e = i % nn, r = e / n, c = e % n;
+        p.theta_out[size_t(sys) * K * nn + i] = sTi[size_t(b) * NN + r * NP + c];
+      }
+      for (int i = tid; i < K * n; i += kSmallThreads)
+        p.gamma_out[size_t(sys) * K * n + i] = sG[(i / n) * NP + i % n];
+      continue;
+    }
+
     // ================================================================ P
     if (tm) tm[3] = small_gtimer();
     small_pcg<T, NP, kSmallThreads>(p, sys, n, K, sD, sL, sTi, sG, U);
