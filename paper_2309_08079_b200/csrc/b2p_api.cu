@@ -1260,28 +1260,35 @@ int b2p_pcg_solve(b2p_ctx* c, int dtype, int K, int nb, const void* S, int kind,
     check_ctx(c);
     const size_t es = esize(dtype), nn = size_t(nb) * nb, D = size_t(dim);
     cudaStream_t st = c->stream();
-    char* dS = static_cast<char*>(ws_get(c, "pc_S", es * K * 3 * nn));
-    char* dP = kind != B2P_IDENTITY ? static_cast<char*>(ws_get(c, "pc_P", es * K * 3 * nn))
-                                    : nullptr;
-    char* dg = static_cast<char*>(ws_get(c, "pc_g", es * D));
-    char* dl0 = static_cast<char*>(ws_get(c, "pc_l0", es * D));
-    char* dl = static_cast<char*>(ws_get(c, "pc_l", es * D));
-    SysOut* dout = static_cast<SysOut*>(ws_get(c, "pc_out", sizeof(SysOut)));
-    h2d(c, dS, S, es * K * 3 * nn, st);
-    if (dP) h2d(c, dP, phi_inv, es * K * 3 * nn, st);
-    h2d(c, dg, gamma, es * D, st);
-    h2d(c, dl0, lambda0, es * D, st);
-    // asymmetry check on device (validate_inputs :42-46)
-    double* d2 = static_cast<double*>(ws_get(c, "pc_ck", 2 * sizeof(double)));
+    // Inputs [S | Phi | gamma | lambda0] packed into one pinned staging block and
+    // sent with one copy; outputs [check | SysOut | lambda] back with one copy.
+    const size_t bS = es * K * 3 * nn, bP = kind != B2P_IDENTITY ? bS : 0, bv = es * D;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t iP = up(bS), ig = iP + up(bP), il0 = ig + up(bv), ibytes = il0 + bv;
+    char* din = static_cast<char*>(ws_get(c, "pc_in", ibytes));
+    char* hin = static_cast<char*>(hws_get(c, "pc_hin", ibytes));
+    std::memcpy(hin, S, bS);
+    if (bP) std::memcpy(hin + iP, phi_inv, bP);
+    std::memcpy(hin + ig, gamma, bv);
+    std::memcpy(hin + il0, lambda0, bv);
+    h2d(c, din, hin, ibytes, st);
+    char* dS = din;
+    char* dP = bP ? din + iP : nullptr;
+    char* dg = din + ig;
+    char* dl0 = din + il0;
+    const size_t oOut = 256, oL = 512, obytes = oL + bv;
+    char* dob = static_cast<char*>(ws_get(c, "pc_ob", obytes));
+    char* hob = static_cast<char*>(hws_get(c, "pc_hob", obytes));
+    char* dl = dob + oL;
+    SysOut* dout = reinterpret_cast<SysOut*>(dob + oOut);
+    // asymmetry check on device (validate_inputs :42-46); evaluated after the
+    // solve's single synchronisation, and reported first, as the reference's
+    // validation precedes the solve
+    double* d2 = reinterpret_cast<double*>(dob);
     CK(cudaMemsetAsync(d2, 0, 2 * sizeof(double), st));
     if (dtype == B2P_F64) CK(launch_blocktri_check<double>(K, nb, (double*)dS, d2, st));
     else CK(launch_blocktri_check<float>(K, nb, (float*)dS, d2, st));
     c->launches++;
-    double ck[2];
-    d2h(c, ck, d2, sizeof(ck), st);
-    CK(cudaStreamSynchronize(st));
-    if (ck[0] > 1e-9 * std::max(1.0, ck[1]))
-      throw invalid("pcg: S is not structurally symmetric (asymmetry " + fstr(ck[0]) + ")");
     int trace_cap = 0;
     double* dtr = nullptr;
     const int mi = (cfg && cfg->max_iter > 0) ? cfg->max_iter : dim;
@@ -1312,12 +1319,17 @@ int b2p_pcg_solve(b2p_ctx* c, int dtype, int K, int nb, const void* S, int kind,
     };
     if (dtype == B2P_F64) go(double{});
     else go(float{});
-    SysOut o;
-    d2h(c, &o, dout, sizeof(SysOut), st);
-    d2h(c, lambda_out, dl, es * D, st);
+    d2h(c, hob, dob, obytes, st);
     CK(cudaStreamSynchronize(st));
     CK(cudaEventElapsedTime(&c->last_ms, c->ev0, c->ev1));
+    double ck[2];
+    std::memcpy(ck, hob, sizeof(ck));
+    if (ck[0] > 1e-9 * std::max(1.0, ck[1]))
+      throw invalid("pcg: S is not structurally symmetric (asymmetry " + fstr(ck[0]) + ")");
+    SysOut o;
+    std::memcpy(&o, hob + oOut, sizeof(SysOut));
     if (o.code != kOk) throw pcg_fail(o);
+    std::memcpy(lambda_out, hob + oL, bv);
     if (dtr && o.trace_len > 0) CK(cudaMemcpy(trace, dtr, sizeof(double) * o.trace_len,
                                              cudaMemcpyDeviceToHost));
     fill_report(report, o, c->last_ms * 1e-3);
