@@ -1162,11 +1162,17 @@ int b2p_build_preconditioner(b2p_ctx* c, int dtype, int kind, int order, int K, 
     check_ctx(c);
     const size_t es = esize(dtype), nn = size_t(nb) * nb;
     cudaStream_t st = c->stream();
-    char* dS = static_cast<char*>(ws_get(c, "bp_S", es * K * 3 * nn));
-    char* dt = static_cast<char*>(ws_get(c, "bp_t", es * K * nn));
-    char* dP = static_cast<char*>(ws_get(c, "bp_P", es * K * 3 * nn));
-    h2d(c, dS, S, es * K * 3 * nn, st);
-    h2d(c, dt, theta_inv, es * K * nn, st);
+    // [S | theta^-1] in one pinned staging block, one copy each way
+    const size_t bS = es * K * 3 * nn, bt = es * K * nn, it = (bS + 255) / 256 * 256;
+    char* din = static_cast<char*>(ws_get(c, "bp_in", it + bt));
+    char* hin = static_cast<char*>(hws_get(c, "bp_hin", it + bt));
+    std::memcpy(hin, S, bS);
+    std::memcpy(hin + it, theta_inv, bt);
+    h2d(c, din, hin, it + bt, st);
+    char* dS = din;
+    char* dt = din + it;
+    char* dP = static_cast<char*>(ws_get(c, "bp_P", bS));
+    char* hP = static_cast<char*>(hws_get(c, "bp_hP", bS));
     if (dtype == B2P_F64) {
       PrecondParams<double> p{1, K, nb, kind, (double*)dS, (double*)dt, (double*)dP};
       CK(launch_build_precond<double>(p, st));
@@ -1175,8 +1181,9 @@ int b2p_build_preconditioner(b2p_ctx* c, int dtype, int kind, int order, int K, 
       CK(launch_build_precond<float>(p, st));
     }
     c->launches++;
-    d2h(c, phi_inv, dP, es * K * 3 * nn, st);
+    d2h(c, hP, dP, bS, st);
     CK(cudaStreamSynchronize(st));
+    std::memcpy(phi_inv, hP, bS);
   });
 }
 
