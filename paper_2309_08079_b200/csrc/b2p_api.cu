@@ -252,8 +252,8 @@ void configure_pcg(b2p_ctx* c, PcgParams<T>& p, bool allow_grid) {
   }
   if (forceStage != 0 && p.B == 1 && static_cast<long long>(p.K) * p.nb > 256) {
     // one system that is not tiny: clusters of 8 or 16 CTAs with <= 112 scalar
-    // rows each measured best (scripts/explicit_policy_probe.py: c1 105 -> 83 us,
-    // K 64 124 -> 99, c2 134 -> 123, K 129 n 4 91 -> 79); longer horizons keep
+    // rows each measured best (scripts/explicit_policy_probe.py: c1 105 -> 78 us,
+    // K 64 124 -> 90, c2 134 -> 121, K 129 n 4 91 -> 70); longer horizons keep
     // the rules below
     const long long rows = static_cast<long long>(p.K) * p.nb;
     const int pref = rows <= 8 * 112 ? 8 : (rows <= 16 * 112 ? 16 : 0);
