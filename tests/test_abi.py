@@ -67,3 +67,18 @@ def test_no_device_means_loud_failure():
         api.require_device()
     with pytest.raises(Exception):
         api.context()
+
+
+def test_argument_validation_before_any_device_work():
+    """Entry points added for the SQP caller and the direct baseline reject bad
+    arguments with INVALID_ARGUMENT and the message, before touching a device."""
+    import ctypes as C
+    L = _lib.load()
+    err = _abi.ErrorC()
+    assert L.b2p_direct_solve_batched_device(None, 0, 1, None, None, None, C.byref(err)) == 1
+    assert b"kkt" in err.message
+    assert L.b2p_uniform_draws(1, -1, 0.0, 1.0, None, C.byref(err)) == 1
+    assert b"uniform_draws" in err.message
+    out = np.zeros(4)
+    assert L.b2p_uniform_draws(7, 4, -1.0, 1.0, out.ctypes.data, C.byref(err)) == 0
+    assert np.all(np.abs(out) <= 1.0) and len(set(out.tolist())) == 4
