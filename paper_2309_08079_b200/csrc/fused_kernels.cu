@@ -292,12 +292,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         const bool kv = k < K;
         const int kc = kv ? k : K - 1;
         T a[NB], x[NB];
-        const T* Qr = sQi + static_cast<size_t>(kc) * nn + lr * NB;
+        // clamped duplicates (k >= K) read Q_{K-1} from global memory: its
+        // shared-memory copy is being inverted in place by its owner
+        if (kv) {
+          const T* Qr = sQi + static_cast<size_t>(kc) * nn + lr * NB;
 #pragma unroll
-        for (int i = 0; i < NB; i += 2) {
-          const double2 q2 = *reinterpret_cast<const double2*>(Qr + i);
-          a[i] = q2.x;
-          a[i + 1] = q2.y;
+          for (int i = 0; i < NB; i += 2) {
+            const double2 q2 = *reinterpret_cast<const double2*>(Qr + i);
+            a[i] = q2.x;
+            a[i + 1] = q2.y;
+          }
+        } else {
+          const T* Qr = Qs + static_cast<size_t>(kc) * nn + lr * NB;
+#pragma unroll
+          for (int i = 0; i < NB; i += 2) {
+            const double2 q2 = __ldg(reinterpret_cast<const double2*>(Qr + i));
+            a[i] = q2.x;
+            a[i + 1] = q2.y;
+          }
         }
         const int f = hw_spd_inverse_v2<T, NB, true>(a, tW, tX, rd, l, x);
         __syncwarp();  // every lane has consumed its Q_k row: overwrite in place

@@ -36,6 +36,7 @@ __device__ __forceinline__ void tstore(T* __restrict__ g, Tile<T> M, int rows, i
     const T v = transpose ? M(j, i) : M(i, j);
     g[idx] = negate ? -v : v;
   }
+  __syncwarp();  // every lane has read the tile before anyone reuses it
 }
 
 template <class T>

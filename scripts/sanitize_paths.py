@@ -31,3 +31,21 @@ for name, env, (N, n, m), dt in cases:
 kb = api.random_kkt_batch(9, 3, 31, 14, 7)
 lam, reps = api.solve_batched(kb, cfg=cfg)
 print("batched one-CTA", api.context().last_path(), [x.iterations for x in reps])
+kb = api.random_kkt_batch(10, 5, 32, 2, 1)  # the small kernel's throughput build
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("batched small-block", api.context().last_path(), [x.iterations for x in reps])
+for (N, n, m) in [(20, 3, 2), (31, 14, 7)]:  # build_schur (small formation-only / fused) +
+    k = api.random_kkt(12, N, n, m)          # build_preconditioner + explicit-Phi pcg_solve
+    sch = api.build_schur(k)
+    P = api.build_preconditioner(sch, PrecondKind.symmetric_stair)
+    r = api.pcg_solve_auto(sch.S, P, sch.gamma, sch.gamma * 0, cfg)
+    print("explicit api", (N, n, m), r.report.iterations)
+import torch  # noqa: E402
+from paper_2309_08079_b200.types import KKTSystem  # noqa: E402
+kb = api.random_kkt_batch(13, 2, 15, 14, 7)
+kd = KKTSystem(15, 14, 7, *[torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in kb.arrays()])
+lam = torch.empty((2, 16 * 14), dtype=torch.float64, device="cuda")
+st = torch.empty((2,), dtype=torch.int32, device="cuda")
+api.direct_solve_batched_device(kd, lam.data_ptr(), st.data_ptr(), 2)
+torch.cuda.synchronize()
+print("direct baseline", st.cpu().tolist())
