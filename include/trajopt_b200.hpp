@@ -174,7 +174,60 @@ struct KKTSystem {
   int N = 0, n = 0, m = 0;
   std::vector<KnotData> knots;  // N+1
   Vector x_s, x0;
+  int primal_dim() const { return (N + 1) * n + N * m; }
   int dual_dim() const { return (N + 1) * n; }
+  /// kkt.cpp:32-39 — c_0 = x_s - x_0, c_{k+1} = -e_k.
+  Vector constraint_rhs() const {
+    Vector c(static_cast<size_t>(dual_dim()));
+    for (int i = 0; i < n; ++i) c[i] = x_s[i] - x0[i];
+    for (int k = 0; k < N; ++k)
+      for (int i = 0; i < n; ++i) c[static_cast<size_t>(k + 1) * n + i] = -knots[k].e[i];
+    return c;
+  }
+  // Dense realizations (kkt.cpp:41-81; oracle bridges for small instances).
+  Matrix dense_G() const {
+    Matrix G(primal_dim(), primal_dim());
+    int off = 0;
+    for (int k = 0; k <= N; ++k) {
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) G(off + i, off + j) = knots[k].Q(i, j);
+      off += n;
+      if (k < N) {
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < m; ++j) G(off + i, off + j) = knots[k].R(i, j);
+        off += m;
+      }
+    }
+    return G;
+  }
+  Vector dense_g() const {
+    Vector g;
+    for (int k = 0; k <= N; ++k) {
+      g.insert(g.end(), knots[k].q.begin(), knots[k].q.end());
+      if (k < N) g.insert(g.end(), knots[k].r.begin(), knots[k].r.end());
+    }
+    return g;
+  }
+  Matrix dense_C() const {
+    Matrix C(dual_dim(), primal_dim());
+    for (int i = 0; i < n; ++i) C(i, i) = 1.0;
+    const int stride = n + m;
+    for (int k = 0; k < N; ++k) {
+      const int row = (k + 1) * n, col = k * stride;
+      for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) C(row + i, col + j) = -knots[k].A(i, j);
+        for (int j = 0; j < m; ++j) C(row + i, col + n + j) = -knots[k].B(i, j);
+        C(row + i, col + stride + i) = 1.0;
+      }
+    }
+    return C;
+  }
+};
+
+/// kkt.hpp — primal update dz = [dx_0 du_0 ... dx_N] and multipliers lambda.
+struct PrimalDual {
+  Vector dz;
+  Vector lambda;
 };
 
 /// SoA buffers in the b2p_kkt layout.

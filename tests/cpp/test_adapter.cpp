@@ -24,7 +24,20 @@ static BlockTriMatrix identity_system(int blocks, int nb) {  // test_pcg.cpp:18-
   return S;
 }
 
+static void kkt_helpers() {  // kkt.cpp:32-81 on a random instance: C dz = c at the exact solve
+  const KKTSystem k = random_kkt(41, 5, 3, 2);
+  const Matrix G = k.dense_G(), C = k.dense_C();
+  const Vector g = k.dense_g(), c = k.constraint_rhs();
+  CHECK(G.rows == k.primal_dim() && C.rows == k.dual_dim() && C.cols == k.primal_dim());
+  CHECK(static_cast<int>(g.size()) == k.primal_dim() && static_cast<int>(c.size()) == k.dual_dim());
+  for (int i = 0; i < k.n; ++i) CHECK(c[i] == k.x_s[i] - k.x0[i]);
+  CHECK(c[static_cast<size_t>(k.n)] == -k.knots[0].e[0]);
+  CHECK(C(0, 0) == 1.0 && C(k.n, 0) == -k.knots[0].A(0, 0));
+  CHECK(G(0, 0) == k.knots[0].Q(0, 0) && G(k.n, k.n) == k.knots[0].R(0, 0));
+}
+
 int main() {
+  kkt_helpers();
   {  // test_pcg.cpp:47-60 — scalar 2x2 within two iterations
     BlockTriMatrix S(2, 1);
     Matrix two = Matrix::identity(1);
