@@ -1,0 +1,77 @@
+"""Parity at scale: per-system PCG iteration counts and lambda agreement between the
+B200 path and the CPU oracle over many seeded systems of every BASELINE config and
+preconditioner (test infrastructure: the oracle is the checker).
+
+  python scripts/parity_sweep.py [out.json]
+
+c4: the full 4096-system bench batch (symstair, eps 1e-8) plus 1024 systems each for
+jacobi / stair / symstair at eps 1e-4; c1 / c3 / NMPC shapes: 256 seeds; c2: 64; c5: 8.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import numpy as np  # noqa: E402
+import pyoracle as orc  # noqa: E402
+import paper_2309_08079_b200.api as api  # noqa: E402
+from paper_2309_08079_b200.types import PcgConfig, PrecondKind  # noqa: E402
+
+orc.build()
+api.require_device()
+KINDS = {"symstair": PrecondKind.symmetric_stair, "stair": PrecondKind.stair,
+         "jacobi": PrecondKind.block_jacobi}
+
+
+def sweep(name, seed0, B, N, n, m, kind, eps, dtype=np.float64):
+    kb = api.random_kkt_batch(seed0, B, N, n, m)
+    cfg = PcgConfig(epsilon=eps)
+    t0 = time.time()
+    lam, reps = api.solve_batched(kb, KINDS[kind], 1, cfg, dtype=dtype)
+    t_gpu = time.time() - t0
+    _, lam_o, reps_o = orc.solve_batch(kb, KINDS[kind], 1, cfg, dtype=dtype)
+    it_g = np.array([r.iterations for r in reps])
+    it_o = np.array([r.iterations for r in reps_o])
+    conv = np.array([r.converged == ro.converged for r, ro in zip(reps, reps_o)])
+    scale = np.maximum(1.0, np.abs(lam_o).max(axis=1))
+    rel = np.abs(lam - lam_o).max(axis=1) / scale
+    diff = np.nonzero(it_g != it_o)[0]
+    margins = [float(reps_o[i].exit_eta / eps) for i in diff[:8]]
+    return {"config": name, "systems": B, "knots": N + 1, "nx": n, "nu": m,
+            "precond": kind, "epsilon": eps, "dtype": np.dtype(dtype).name,
+            "iterations_equal": int((it_g == it_o).sum()),
+            "iteration_mismatches": [int(i) for i in diff[:8]],
+            "mismatch_oracle_exit_eta_over_eps": margins,
+            "converged_equal": int(conv.sum()),
+            "lambda_rel_err_max": float(rel.max()), "lambda_rel_err_median": float(np.median(rel)),
+            "iters_mean": float(it_o.mean()), "gpu_wall_s": t_gpu}
+
+
+def main():
+    out = []
+    plan = [
+        ("c4", 2309, 4096, 63, 14, 7, "symstair", 1e-8, np.float64),
+        ("c4", 4000, 1024, 63, 14, 7, "symstair", 1e-4, np.float64),
+        ("c4", 5000, 1024, 63, 14, 7, "stair", 1e-4, np.float64),
+        ("c4", 6000, 1024, 63, 14, 7, "jacobi", 1e-4, np.float64),
+        ("c1", 100, 256, 31, 14, 7, "symstair", 1e-8, np.float64),
+        ("c1", 200, 256, 31, 14, 7, "stair", 1e-8, np.float64),
+        ("c2", 300, 64, 127, 14, 7, "symstair", 1e-8, np.float64),
+        ("c3", 400, 256, 255, 12, 4, "symstair", 1e-4, np.float32),
+        ("c5", 500, 8, 511, 28, 14, "symstair", 1e-8, np.float64),
+        ("nmpc_n2", 600, 256, 32, 2, 1, "symstair", 1e-8, np.float64),
+        ("nmpc_n4", 700, 256, 32, 4, 1, "symstair", 1e-8, np.float64),
+    ]
+    for args in plan:
+        r = sweep(*args)
+        print(json.dumps(r), flush=True)
+        out.append(r)
+    path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/parity_sweep.json"
+    json.dump({"what": __doc__.strip().splitlines()[0], "rows": out}, open(path, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
