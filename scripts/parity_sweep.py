@@ -23,7 +23,7 @@ from paper_2309_08079_b200.types import PcgConfig, PrecondKind  # noqa: E402
 orc.build()
 api.require_device()
 KINDS = {"symstair": PrecondKind.symmetric_stair, "stair": PrecondKind.stair,
-         "jacobi": PrecondKind.block_jacobi}
+         "jacobi": PrecondKind.block_jacobi, "identity": PrecondKind.identity}
 
 
 def sweep(name, seed0, B, N, n, m, kind, eps, dtype=np.float64):
@@ -40,7 +40,21 @@ def sweep(name, seed0, B, N, n, m, kind, eps, dtype=np.float64):
     rel = np.abs(lam - lam_o).max(axis=1) / scale
     diff = np.nonzero(it_g != it_o)[0]
     margins = [float(reps_o[i].exit_eta / eps) for i in diff[:8]]
-    return {"config": name, "systems": B, "knots": N + 1, "nx": n, "nu": m,
+    off = np.abs(it_g - it_o)
+    extra = {}
+    if kind == "identity":
+        # the reference's own block-parallel variant (deterministic tree reductions,
+        # pcg.cpp:157-362) on the same systems: how far its counts sit from the
+        # sequential variant's, and whether the B200 count is within one of either
+        _, _, reps_p = orc.solve_batch(kb, KINDS[kind], 1, PcgConfig(
+            epsilon=eps, variant=1, deterministic_reductions=True), dtype=dtype)
+        it_p = np.array([r.iterations for r in reps_p])
+        within = np.minimum(np.abs(it_g - it_o), np.abs(it_g - it_p)) <= 1
+        extra = {"oracle_variants_differ": int((it_o != it_p).sum()),
+                 "oracle_variants_max_diff": int(np.abs(it_o - it_p).max()),
+                 "b200_within_one_of_either_variant": int(within.sum())}
+    return {"config": name, "systems": B, "knots": N + 1, "nx": n, "nu": m, **extra,
+            "iterations_off_by_one": int((off == 1).sum()), "iterations_off_more": int((off > 1).sum()),
             "precond": kind, "epsilon": eps, "dtype": np.dtype(dtype).name,
             "iterations_equal": int((it_g == it_o).sum()),
             "iteration_mismatches": [int(i) for i in diff[:8]],
@@ -64,6 +78,9 @@ def main():
         ("c5", 500, 8, 511, 28, 14, "symstair", 1e-8, np.float64),
         ("nmpc_n2", 600, 256, 32, 2, 1, "symstair", 1e-8, np.float64),
         ("nmpc_n4", 700, 256, 32, 4, 1, "symstair", 1e-8, np.float64),
+        # unpreconditioned CG (80-95 steps on kappa ~ 1e4): the documented +-1 policy
+        ("c1", 800, 256, 31, 14, 7, "identity", 1e-8, np.float64),
+        ("c4", 900, 256, 63, 14, 7, "identity", 1e-8, np.float64),
     ]
     for args in plan:
         r = sweep(*args)
