@@ -292,7 +292,7 @@ def pcg_solve_auto(S: BlockTriMatrix, P: Preconditioner, gamma, lambda0,
         pK, pnb = phi.shape[0], phi.shape[2]
     lam = np.zeros(max(K * nb, 1), dtype=dt)
     rep = _abi.SolveReportC()
-    trace = np.zeros(max(1, _max_iter(cfg, K * nb)))
+    trace = np.zeros(max(1, _max_iter(cfg, K * nb))) if cfg.collect_trace else None
     err = _abi.ErrorC()
     c = cfg.to_c()
     _check(load().b2p_pcg_solve(context().handle, _dt(dt), K, nb, _ptr(d), int(P.kind),
@@ -323,7 +323,7 @@ def solve(kkt: KKTSystem, kind=PrecondKind.symmetric_stair, order: int = 1,
     lam = np.zeros(D, dtype=dt)
     l0 = None if lambda0 is None else _arr(lambda0, dt)
     rep = _abi.SolveReportC()
-    trace = np.zeros(max(1, _max_iter(cfg, D)))
+    trace = np.zeros(max(1, _max_iter(cfg, D))) if cfg.collect_trace else None
     err = _abi.ErrorC()
     c = cfg.to_c()
     _check(load().b2p_solve(context().handle, _dt(dt), C.byref(k.to_c()), int(kind), int(order),
@@ -398,7 +398,7 @@ def sqp_step(kkt: KKTSystem, kind=PrecondKind.symmetric_stair, order: int = 1,
     dz = np.zeros(k.primal_dim(), dtype=dt)
     l0 = None if lambda0 is None else _arr(lambda0, dt)
     rep = _abi.SolveReportC()
-    trace = np.zeros(max(1, _max_iter(cfg, D)))
+    trace = np.zeros(max(1, _max_iter(cfg, D))) if cfg.collect_trace else None
     err = _abi.ErrorC()
     c = cfg.to_c()
     _check(load().b2p_sqp_step(context().handle, _dt(dt), C.byref(k.to_c()), int(kind),
