@@ -47,3 +47,8 @@ def test_b200_arm_contract():
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] > 0
     for c in ("c1", "c2", "c3", "c5"):
         assert d["latency"][c]["us_median"] > 0
+    # the reference's other bench rows and callers: direct baseline, SQP step, NMPC batch
+    assert d["dense_baseline"]["all_ok"] and d["dense_baseline"]["max_rel_diff_vs_pcg"] < 1e-3
+    assert d["latency"]["sqp_step_n2"]["kernel"] == "fused small"
+    assert d["latency"]["nmpc_batch_n2"]["systems_per_s"] > 0
+    assert d["roofline"]["onchip"]["l1tex_throughput_pct_of_peak"] > 0
