@@ -23,16 +23,18 @@ from paper_2309_08079_b200.types import PcgConfig, PrecondKind  # noqa: E402
 orc.build()
 api.require_device()
 KINDS = {"symstair": PrecondKind.symmetric_stair, "stair": PrecondKind.stair,
-         "jacobi": PrecondKind.block_jacobi, "identity": PrecondKind.identity}
+         "jacobi": PrecondKind.block_jacobi, "identity": PrecondKind.identity,
+         "poly:1": PrecondKind.poly_split, "poly:2": PrecondKind.poly_split}
 
 
 def sweep(name, seed0, B, N, n, m, kind, eps, dtype=np.float64):
     kb = api.random_kkt_batch(seed0, B, N, n, m)
     cfg = PcgConfig(epsilon=eps)
     t0 = time.time()
-    lam, reps = api.solve_batched(kb, KINDS[kind], 1, cfg, dtype=dtype)
+    order = int(kind.split(":")[1]) if kind.startswith("poly") else 1
+    lam, reps = api.solve_batched(kb, KINDS[kind], order, cfg, dtype=dtype)
     t_gpu = time.time() - t0
-    _, lam_o, reps_o = orc.solve_batch(kb, KINDS[kind], 1, cfg, dtype=dtype)
+    _, lam_o, reps_o = orc.solve_batch(kb, KINDS[kind], order, cfg, dtype=dtype)
     it_g = np.array([r.iterations for r in reps])
     it_o = np.array([r.iterations for r in reps_o])
     conv = np.array([r.converged == ro.converged for r, ro in zip(reps, reps_o)])
@@ -74,6 +76,10 @@ def main():
         ("c1", 100, 256, 31, 14, 7, "symstair", 1e-8, np.float64),
         ("c1", 200, 256, 31, 14, 7, "stair", 1e-8, np.float64),
         ("c2", 300, 64, 127, 14, 7, "symstair", 1e-8, np.float64),
+        ("c2", 310, 64, 127, 14, 7, "stair", 1e-8, np.float64),
+        ("c2", 320, 64, 127, 14, 7, "jacobi", 1e-8, np.float64),
+        ("c1", 330, 128, 31, 14, 7, "poly:1", 1e-8, np.float64),
+        ("c1", 340, 128, 31, 14, 7, "poly:2", 1e-8, np.float64),
         ("c3", 400, 256, 255, 12, 4, "symstair", 1e-4, np.float32),
         ("c5", 500, 8, 511, 28, 14, "symstair", 1e-8, np.float64),
         ("nmpc_n2", 600, 256, 32, 2, 1, "symstair", 1e-8, np.float64),
