@@ -221,12 +221,12 @@ def run_reference(a, world, rank):
 
 
 # ------------------------------------------------------------------ GPU arm
-def c1_graph_latency(api, torch, local, reps=200):
+def c1_graph_latency(api, torch, local, reps=200, N=31, n=14, m=7):
     from paper_2309_08079_b200.types import KKTSystem
-    kk = api.random_kkt(1, 31, 14, 7)
+    kk = api.random_kkt(1, N, n, m)
     dev = [torch.from_numpy(np.ascontiguousarray(x)[None]).to(f"cuda:{local}") for x in kk.arrays()]
-    kd = KKTSystem(31, 14, 7, *dev)
-    lam = torch.empty((1, 32 * 14), dtype=torch.float64, device=f"cuda:{local}")
+    kd = KKTSystem(N, n, m, *dev)
+    lam = torch.empty((1, (N + 1) * n), dtype=torch.float64, device=f"cuda:{local}")
     ctx = api.Context(local)
     s = torch.cuda.Stream(device=local)
     ctx.set_stream(s.cuda_stream)
@@ -428,6 +428,10 @@ def run_b200(a, world, rank, local):
             latency["c1_graph"] = c1_graph_latency(api, torch, local)
         except Exception as exc:  # report, do not fail the bench line
             latency["c1_graph"] = {"error": str(exc)[:200]}
+        try:  # the NMPC-shape single solve replayed from a CUDA graph (launch floor)
+            latency["nmpc_graph_n2"] = c1_graph_latency(api, torch, local, N=32, n=2, m=1)
+        except Exception as exc:
+            latency["nmpc_graph_n2"] = {"error": str(exc)[:200]}
         try:
             latency["nmpc_batch_n2"] = nmpc_batch_throughput(api, torch, local)
         except Exception as exc:
