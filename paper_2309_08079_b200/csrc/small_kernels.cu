@@ -29,7 +29,10 @@
 namespace b2p {
 namespace {
 
-constexpr int kSmallThreads = 256;
+// CTA size: 128 threads when the padded system has <= 128 scalar rows (n <= 2
+// at the NMPC horizons: fewer warps in every barrier and reduction, twice the
+// CTAs per SM in batches), else 256
+constexpr int kSmallThreadsLo = 128, kSmallThreadsHi = 256;
 // lanes per block-row group: the padded block size (>= 2), so n <= 2 packs 128
 // groups per CTA and a K = 33 horizon forms in one trip instead of two
 template <int NP, int MP>
@@ -37,10 +40,10 @@ constexpr int group_width() {
   return (NP > MP ? NP : MP) < 2 ? 2 : (NP > MP ? NP : MP);
 }
 
-template <int NP, int MP>
+template <int NP, int MP, int TH>
 struct SmallLayout {
   static constexpr int NN = NP * NP, MM = MP * MP;
-  static constexpr int GW = group_width<NP, MP>(), kGroups = kSmallThreads / GW;
+  static constexpr int GW = group_width<NP, MP>(), kGroups = TH / GW;
   // per lane group: Lr, LiT, sym tile, rd (n-sized) + Lr, LiT, rd (m-sized)
   static constexpr int tile = 3 * NN + NP + 2 * MM + MP;
 };
@@ -280,11 +283,11 @@ __device__ void small_pcg(const FusedParams<T>& p, int sys, int n, int K, const 
 // BATCH = true: the throughput build for batches (registers capped so 4 / 3 CTAs
 // fit an SM at n <= 2 / 4: 11.6 -> 15.6 M systems/s at n = 2); BATCH = false:
 // the latency build for single solves (uncapped registers: 30.6 vs 34 us).
-template <class T, int NP, int MP, bool BATCH>
+template <class T, int NP, int MP, bool BATCH, int kSmallThreads>
 __global__ void __launch_bounds__(kSmallThreads, (!BATCH ? 1 : (NP <= 2 ? 4 : (NP <= 4 ? 3 : 1))))
     k_fused_small(FusedParams<T> p, int n, int m,
                                                                int staged) {
-  using L = SmallLayout<NP, MP>;
+  using L = SmallLayout<NP, MP, kSmallThreads>;
   constexpr int NN = L::NN, MM = L::MM;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* smem = reinterpret_cast<T*>(smem_raw);
@@ -550,34 +553,43 @@ int pad_pow2(int v) { return v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : v <= 8 ? 8 :
 // [K][NP], then the formation scratch (Q^-1, Q^-1 q, R^-1, R^-1 r, the
 // per-group inverse tiles and, when `staged`, the system's knot data) aliased
 // by the PCG vectors.
-size_t small_bytes_rt(int NP, int MP, int K, bool staged) {
+size_t small_bytes_rt(int NP, int MP, int K, bool staged, int threads) {
   const size_t NN = size_t(NP) * NP, MM = size_t(MP) * MP, N = K > 1 ? K - 1 : 0;
   const int GW = std::max(2, std::max(NP, MP));
   const size_t tile = 3 * NN + NP + 2 * MM + MP;
   const size_t stg =
       staged ? size_t(K) * (NN + NP) + N * (MM + MP + NN + NP * MP + NP) + 2 * NP : 0;
   const size_t form_t = size_t(K) * (NN + NP) + std::max<size_t>(N, 1) * (MM + MP) +
-                        size_t(kSmallThreads / GW) * tile + stg;
+                        size_t(threads / GW) * tile + stg;
   const size_t pcg = size_t(8) * K * NP + 64;
   return sizeof(double) * (size_t(K) * (3 * NN + NP) + std::max(form_t, pcg));
 }
 
+int small_threads(int NP, int K) { return K * NP <= 128 ? kSmallThreadsLo : kSmallThreadsHi; }
+
 constexpr size_t kSmallSmemCap = 227 * 1024 - 1024;
 
-template <class T, int NP, int MP>
-cudaError_t go_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
-  const bool staged = small_bytes_rt(NP, MP, p.K, true) <= kSmallSmemCap;
-  const size_t smem = small_bytes_rt(NP, MP, p.K, staged);
-  auto kern = p.B > 1 ? k_fused_small<T, NP, MP, true> : k_fused_small<T, NP, MP, false>;
+template <class T, int NP, int MP, int TH>
+cudaError_t go_small_th(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
+  const bool staged = small_bytes_rt(NP, MP, p.K, true, TH) <= kSmallSmemCap;
+  const size_t smem = small_bytes_rt(NP, MP, p.K, staged, TH);
+  auto kern = p.B > 1 ? k_fused_small<T, NP, MP, true, TH> : k_fused_small<T, NP, MP, false, TH>;
   cudaError_t e = ensure_max_smem(kern, smem);
   if (e != cudaSuccess) return e;
   // persistent CTAs: as many as fit co-resident (`grid` = SM count on entry)
   int per_sm = 1;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmallThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH, smem);
   if (e != cudaSuccess) return e;
   grid = std::max(1, std::min(p.B, grid * std::max(1, per_sm)));
-  kern<<<grid, kSmallThreads, smem, st>>>(p, n, m, staged ? 1 : 0);
+  kern<<<grid, TH, smem, st>>>(p, n, m, staged ? 1 : 0);
   return cudaGetLastError();
+}
+
+template <class T, int NP, int MP>
+cudaError_t go_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
+  if (small_threads(NP, p.K) == kSmallThreadsLo)
+    return go_small_th<T, NP, MP, kSmallThreadsLo>(p, n, m, grid, st);
+  return go_small_th<T, NP, MP, kSmallThreadsHi>(p, n, m, grid, st);
 }
 
 template <class T, int NP>
@@ -597,7 +609,8 @@ template <class T>
 bool small_supported(int K, int n, int m, int kind) {
   if (sizeof(T) != 8 || kind == kPoly) return false;
   if (n < 1 || n > 8 || m < 1 || m > 8 || K < 1) return false;
-  return small_bytes_rt(pad_pow2(n), pad_pow2(m), K, false) <= kSmallSmemCap;
+  const int NP = pad_pow2(n), MP = pad_pow2(m);
+  return small_bytes_rt(NP, MP, K, false, small_threads(NP, K)) <= kSmallSmemCap;
 }
 
 template <class T>
