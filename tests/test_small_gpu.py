@@ -45,6 +45,18 @@ def test_small_kernel_matches_oracle(api, orc, kind, shape):
     _check(api, orc, kkt, kind, PcgConfig(epsilon=1e-8))
 
 
+@pytest.mark.parametrize("shape", [(999, 2, 1), (2047, 1, 1), (400, 8, 4)])
+def test_small_kernel_long_horizons(api, orc, shape):
+    """Long horizons: more rows than threads (strided rows), unstaged knot data, or
+    beyond the shared-memory bound (then the split path takes over, still exact)."""
+    N, n, m = shape
+    kkt = orc.random_trajectory_kkt(5 + N, N, n, m)
+    cfg = PcgConfig(epsilon=1e-10)
+    got = api.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    want = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    _cmp(got, want, TOL64, cfg.epsilon)
+
+
 @pytest.mark.parametrize("N", [0, 1, 2, 31, 32, 33, 64, 200])
 def test_small_kernel_ragged_horizons(api, orc, N):
     """K = N + 1 around the 32-group trip boundaries, down to the single knot."""
