@@ -251,6 +251,9 @@ struct PackedKKT {
   }
 };
 inline PackedKKT pack(const KKTSystem& s) {
+  if (static_cast<int>(s.knots.size()) != s.N + 1)
+    throw std::invalid_argument("b2p: KKTSystem needs N+1 knots, got " +
+                                std::to_string(s.knots.size()));
   PackedKKT p;
   for (int k = 0; k <= s.N; ++k) {
     const KnotData& kd = s.knots[k];
@@ -266,8 +269,21 @@ inline PackedKKT pack(const KKTSystem& s) {
   }
   p.x_s = s.x_s;
   p.x0 = s.x0;
+  const size_t K = s.N + 1, N = s.N, n = s.n, m = s.m;
+  if (p.Q.size() != K * n * n || p.q.size() != K * n || p.R.size() != N * m * m ||
+      p.r.size() != N * m || p.A.size() != N * n * n || p.B.size() != N * n * m ||
+      p.e.size() != N * n || p.x_s.size() != n || p.x0.size() != n)
+    throw std::invalid_argument("b2p: KKTSystem knot data does not match (N, n, m)");
   return p;
 }
+namespace detail {
+/// pcg.cpp:34-35's message for a lambda0 of the wrong length.
+inline void check_lambda0(const Vector* lambda0, int dim) {
+  if (lambda0 && static_cast<int>(lambda0->size()) != dim)
+    throw std::invalid_argument("pcg: expected lambda0 of length " + std::to_string(dim) +
+                                ", got " + std::to_string(lambda0->size()));
+}
+}  // namespace detail
 
 /// random_problem.cpp:42-80 (host generator in libb2p, the reference's draw order).
 inline KKTSystem random_kkt_family(int family, std::uint64_t seed, int N, int n, int m,
@@ -494,6 +510,7 @@ inline PcgResult pcg_solve_block_parallel(const BlockTriMatrix& S, const Precond
 /// Fused hot path: build_schur -> build_preconditioner -> pcg_solve_auto.
 inline PcgResult solve(const KKTSystem& kkt, PrecondKind kind, int order, const PcgConfig& cfg,
                        const Vector* lambda0 = nullptr) {
+  detail::check_lambda0(lambda0, kkt.dual_dim());
   const PackedKKT p = pack(kkt);
   const b2p_kkt v = p.view(kkt.N, kkt.n, kkt.m);
   const b2p_pcg_config c = detail::to_c(cfg);
@@ -531,6 +548,7 @@ struct SqpStepResult {
 };
 inline SqpStepResult sqp_step(const KKTSystem& kkt, PrecondKind kind, int order,
                               const PcgConfig& cfg, const Vector& lambda0) {
+  if (!lambda0.empty()) detail::check_lambda0(&lambda0, kkt.dual_dim());
   const PackedKKT p = pack(kkt);
   const b2p_kkt v = p.view(kkt.N, kkt.n, kkt.m);
   const b2p_pcg_config c = detail::to_c(cfg);
@@ -554,7 +572,10 @@ inline SqpStepResult sqp_step(const KKTSystem& kkt, PrecondKind kind, int order,
 #if __has_include(<Eigen/Dense>)
 #include <Eigen/Dense>
 namespace trajopt_b200 {
-// Eigen bridge: the reference's callers pass Eigen::VectorXd / MatrixXd.
+// Eigen bridge: the reference's callers pass Eigen::VectorXd / MatrixXd and
+// the Eigen-typed trajopt::KKTSystem (kkt.hpp:13-46). Callers that want the
+// reference's own signatures instead use the drop-in headers under
+// include/trajopt_dropin.
 inline Vector from_eigen(const Eigen::VectorXd& v) { return Vector(v.data(), v.data() + v.size()); }
 inline Eigen::VectorXd to_eigen(const Vector& v) {
   return Eigen::Map<const Eigen::VectorXd>(v.data(), static_cast<Eigen::Index>(v.size()));
@@ -564,6 +585,32 @@ inline Matrix from_eigen(const Eigen::MatrixXd& M) {
   for (int i = 0; i < out.rows; ++i)
     for (int j = 0; j < out.cols; ++j) out(i, j) = M(i, j);  // column-major -> row-major
   return out;
+}
+/// trajopt::KKTSystem (or any type with the reference's field names: N, n, m,
+/// knots[k].{Q,q,R,r,A,B,e}, x_s, x0) -> this adapter's row-major KKTSystem.
+template <class EigenKKT>
+inline KKTSystem to_b200(const EigenKKT& kkt) {
+  KKTSystem s;
+  s.N = kkt.N;
+  s.n = kkt.n;
+  s.m = kkt.m;
+  s.knots.resize(static_cast<size_t>(kkt.N) + 1);
+  for (int k = 0; k <= kkt.N; ++k) {
+    const auto& kd = kkt.knots[k];
+    KnotData& o = s.knots[k];
+    o.Q = from_eigen(Eigen::MatrixXd(kd.Q));
+    o.q = from_eigen(Eigen::VectorXd(kd.q));
+    if (k < kkt.N) {
+      o.R = from_eigen(Eigen::MatrixXd(kd.R));
+      o.r = from_eigen(Eigen::VectorXd(kd.r));
+      o.A = from_eigen(Eigen::MatrixXd(kd.A));
+      o.B = from_eigen(Eigen::MatrixXd(kd.B));
+      o.e = from_eigen(Eigen::VectorXd(kd.e));
+    }
+  }
+  s.x_s = from_eigen(Eigen::VectorXd(kkt.x_s));
+  s.x0 = from_eigen(Eigen::VectorXd(kkt.x0));
+  return s;
 }
 }  // namespace trajopt_b200
 #endif

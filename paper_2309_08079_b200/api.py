@@ -115,6 +115,28 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
+def _check_kkt(k: KKTSystem, batch: int | None = None):
+    """Every array of a host KKTSystem must have the b2p_kkt shape for (N, n, m)
+    (plus the leading batch dimension): the C side reads exactly that many bytes."""
+    shapes = _abi.kkt_shapes(k.N, k.n, k.m)
+    for f in _abi.KKT_FIELDS:
+        a = getattr(k, f)
+        want = shapes[f] if batch is None else (batch,) + shapes[f]
+        if tuple(a.shape) != want:
+            raise ValueError(f"KKTSystem.{f}: expected shape {want}, got {tuple(a.shape)}")
+
+
+def _lambda0(lambda0, dt, dim: int, batch: int | None = None):
+    """lambda0 as a contiguous dt vector of the dual dimension (pcg.cpp:34-35)."""
+    if lambda0 is None:
+        return None
+    l0 = _arr(lambda0, dt)
+    want = dim if batch is None else batch * dim
+    if l0.size != want:
+        raise ValueError(f"pcg: expected lambda0 of length {want}, got {l0.size}")
+    return l0
+
+
 def _compute_dtype(x, dtype):
     if dtype is not None:
         return np.dtype(dtype)
@@ -192,6 +214,7 @@ def cholesky_solve(M: BlockTriMatrix, rhs, dtype=None) -> np.ndarray:
 def build_schur(kkt: KKTSystem, dtype=np.float64) -> SchurSystem:  # schur.cpp:38-82
     dt = np.dtype(dtype)
     k = kkt.astype(dt)
+    _check_kkt(k)
     K, n = k.N + 1, k.n
     S = np.zeros((K, 3, n, n), dtype=dt)
     gamma = np.zeros(K * n, dtype=dt)
@@ -319,9 +342,10 @@ def solve(kkt: KKTSystem, kind=PrecondKind.symmetric_stair, order: int = 1,
     cfg = cfg or PcgConfig()
     dt = np.dtype(dtype)
     k = kkt.astype(dt)
+    _check_kkt(k)
     D = k.dual_dim()
     lam = np.zeros(D, dtype=dt)
-    l0 = None if lambda0 is None else _arr(lambda0, dt)
+    l0 = _lambda0(lambda0, dt, D)
     rep = _abi.SolveReportC()
     trace = np.zeros(max(1, _max_iter(cfg, D))) if cfg.collect_trace else None
     err = _abi.ErrorC()
@@ -342,9 +366,19 @@ def solve_batched(kkt_batch: KKTSystem, kind=PrecondKind.symmetric_stair, order:
     dt = np.dtype(dtype)
     k = kkt_batch if all(a.dtype == dt for a in kkt_batch.arrays()) else kkt_batch.astype(dt)
     B = k.batch
+    if B is None:
+        raise ValueError("solve_batched: kkt_batch needs a leading batch dimension")
+    _check_kkt(k, B)
     D = k.dual_dim()
-    lam = lambda_out if lambda_out is not None else np.zeros((B, D), dtype=dt)
-    l0 = None if lambda0 is None else _arr(lambda0, dt)
+    if lambda_out is not None:
+        if (not isinstance(lambda_out, np.ndarray) or lambda_out.dtype != dt
+                or tuple(lambda_out.shape) != (B, D) or not lambda_out.flags["C_CONTIGUOUS"]):
+            raise ValueError(f"solve_batched: lambda_out must be a C-contiguous {dt.name} "
+                             f"array of shape ({B}, {D})")
+        lam = lambda_out
+    else:
+        lam = np.zeros((B, D), dtype=dt)
+    l0 = _lambda0(lambda0, dt, D, B)
     reps = (_abi.SolveReportC * B)()
     err = _abi.ErrorC()
     c = cfg.to_c()
@@ -358,10 +392,12 @@ def solve_batched(kkt_batch: KKTSystem, kind=PrecondKind.symmetric_stair, order:
 def solve_batched_device(kkt_dev: KKTSystem, lambda_out_ptr: int, batch: int,
                          kind=PrecondKind.symmetric_stair, order: int = 1,
                          cfg: PcgConfig | None = None, lambda0_ptr: int | None = None,
-                         dtype=np.float64, ctx: Context | None = None, want_reports=False):
+                         dtype=np.float64, ctx: Context | None = None, want_reports=False,
+                         status_ptr: int | None = None):
     """Device-resident batch: kkt_dev holds device tensors (anything with
     .data_ptr()). Launches on the context stream; no host sync unless
-    want_reports."""
+    want_reports. status_ptr: optional device int32[batch][4] (16-byte aligned)
+    receiving {status, iterations, converged, aux} per system on the stream."""
     cfg = cfg or PcgConfig()
     ctx = ctx or context()
     kc = kkt_dev.to_c(ptr=lambda t: t.data_ptr())
@@ -370,7 +406,7 @@ def solve_batched_device(kkt_dev: KKTSystem, lambda_out_ptr: int, batch: int,
     c = cfg.to_c()
     _check(load().b2p_solve_batched_device(ctx.handle, _dt(dtype), batch, C.byref(kc),
                                            int(kind), int(order), C.byref(c), lambda0_ptr,
-                                           lambda_out_ptr, reps, None, C.byref(err)), err)
+                                           lambda_out_ptr, reps, status_ptr, C.byref(err)), err)
     return [SolveReport.from_c(r) for r in reps] if want_reports else None
 
 
@@ -378,6 +414,7 @@ def reconstruct_primal(kkt: KKTSystem, lam, dtype=np.float64) -> np.ndarray:  # 
     """dz = [x_0, u_0, ..., x_N] from the multipliers (one warp per knot block)."""
     dt = np.dtype(dtype)
     k = kkt.astype(dt)
+    _check_kkt(k)
     lam = np.ascontiguousarray(np.asarray(lam), dtype=dt).reshape(-1)
     dz = np.zeros(k.primal_dim(), dtype=dt)
     err = _abi.ErrorC()
@@ -395,8 +432,9 @@ def sqp_step(kkt: KKTSystem, kind=PrecondKind.symmetric_stair, order: int = 1,
     k = kkt.astype(dt)
     D = k.dual_dim()
     lam = np.zeros(D, dtype=dt)
+    _check_kkt(k)
     dz = np.zeros(k.primal_dim(), dtype=dt)
-    l0 = None if lambda0 is None else _arr(lambda0, dt)
+    l0 = _lambda0(lambda0, dt, D)
     rep = _abi.SolveReportC()
     trace = np.zeros(max(1, _max_iter(cfg, D))) if cfg.collect_trace else None
     err = _abi.ErrorC()
@@ -435,6 +473,7 @@ def solve_batched_multi(devices, kkt_batch: KKTSystem, kind=PrecondKind.symmetri
     cfg = cfg or PcgConfig()
     dt = np.dtype(dtype)
     k = kkt_batch.astype(dt)
+    _check_kkt(k, k.batch)
     B, D = k.batch, k.dual_dim()
     lam = np.zeros((B, D), dtype=dt)
     reps = (_abi.SolveReportC * B)()

@@ -74,6 +74,35 @@ def build_adapter_test(force: bool = False) -> str:
     return out
 
 
+def build_dropin_test(force: bool = False) -> str:
+    """g++ the drop-in acceptance test (tests/cpp/test_dropin.cpp): the reference's
+    Eigen-typed trajopt:: API (include/trajopt_dropin) against libb2p.so, compiled
+    with the test-only Eigen stand-in; the CPU oracle header is its checker."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "tests", "cpp", "test_dropin.cpp")
+    dropin = os.path.join(root, "include", "trajopt_dropin")
+    hdrs = [os.path.join(dropin, "trajopt", h)
+            for h in ("b200_detail.hpp", "block_tri.hpp", "schur.hpp", "pcg.hpp")]
+    hdrs += [os.path.join(root, "include", "trajopt_b200.hpp"),
+             os.path.join(root, "tests", "cpp", "eigen_stub", "Eigen", "Dense"),
+             os.path.join(root, "tests", "cpp", "ref_stub", "trajopt", "kkt.hpp"),
+             os.path.join(root, "oracle", "trajopt_oracle.hpp")]
+    out = os.path.join(root, "build", "test_dropin")
+    if not force and not _stale(out, [src, LIB] + hdrs):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    # include order as an integrator would set it: the drop-in ahead of the
+    # reference's own include directory (here: its test-only KKT stand-in)
+    subprocess.check_call(["g++", "-std=c++20", "-O2", "-Wall", "-pthread",
+                           "-I", os.path.join(root, "tests", "cpp", "eigen_stub"),
+                           "-I", dropin,
+                           "-I", os.path.join(root, "tests", "cpp", "ref_stub"),
+                           "-I", os.path.join(root, "include"), "-I", os.path.join(root, "oracle"),
+                           src, "-o", out, "-L", HERE, "-lb2p",
+                           "-Wl,-rpath,$ORIGIN/../paper_2309_08079_b200"])
+    return out
+
+
 def build_sqp_test(force: bool = False) -> str:
     """g++ the SQP / NMPC caller tests (tests/cpp/test_sqp.cpp) against libb2p.so.
     The test links the CPU oracle header as its checker (test infrastructure)."""

@@ -38,7 +38,9 @@ struct b2p_ctx {
   std::vector<cudaEvent_t> pool;
   size_t pool_used = 0;
   float last_ms = 0.f;
-  unsigned fg_epoch = 0;  // next LL epoch of the fused grid kernel
+  // next LL epoch of the fused grid kernel, one counter per LL buffer (tag):
+  // a buffer's words are only ever compared against its own epochs
+  std::map<std::string, unsigned> fg_epoch;
   int last_path = 0;  // 0: split K1(+K2)+K3, 1: one-CTA fused, 2: fused cluster, 3: fused grid
   unsigned long long* timing = nullptr;  // B2P_PHASE_TIMING=1: per-system phase stamps
   int timing_n = 0;
@@ -335,13 +337,16 @@ size_t kkt_block_bytes(const b2p_kkt* k, size_t esz, int count) {
 // stream before returning, so the staging block is free again by the next call.
 KktDev upload_kkt(b2p_ctx* c, const b2p_kkt* k, size_t esz, int first, int count, void* dst,
                   cudaStream_t st, const void* extra = nullptr, size_t extra_bytes = 0,
-                  char** extra_dev = nullptr) {
+                  char** extra_dev = nullptr, bool may_stage = true) {
   const size_t N = k->N, n = k->n, m = k->m, K = N + 1;
   const size_t sz[9] = {K * n * n, K * n, N * m * m, N * m, N * n * n, N * n * m, N * n, n, n};
   const void* src[9] = {k->Q, k->q, k->R, k->r, k->A, k->B, k->e, k->x_s, k->x0};
   const void* out[9];
   char* d = static_cast<char*>(dst);
-  const bool staged = count == 1;
+  // the chunked pipeline of b2p_solve_batched does not synchronise between
+  // chunks, so it never stages (one staging block would be overwritten while
+  // an earlier chunk's asynchronous H2D still reads it)
+  const bool staged = count == 1 && may_stage;
   const size_t total = kkt_block_bytes(k, esz, count) + extra_bytes;
   char* h = staged ? static_cast<char*>(hws_get(c, "up_stage", total)) : nullptr;
   for (int a = 0; a < 9; ++a) {
@@ -448,7 +453,8 @@ void launch_form(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, T* S, T*
     g.e = f.e;
     g.x_s = f.x_s;
     g.x0 = f.x0;
-    g.slot = static_cast<T*>(ws_get(c, "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, k->n, k->m)));
+    g.slot = static_cast<T*>(
+        ws_get(c, "form_slot", sizeof(T) * grid * fused_slot_elems<T>(K, k->n, k->m)));
     g.errkey = errkey;
     g.out = static_cast<SysOut*>(ws_get(c, "form_out", sizeof(SysOut) * B));
     g.S_out = S;
@@ -537,12 +543,13 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     unsigned long long* ll = static_cast<unsigned long long*>(ws_get(c, tag + "fg_ll", bytes));
     const unsigned need = static_cast<unsigned>(
         std::min<long long>(1ll << 30, 3ll * (f.max_iter + 4) * B + 16));
-    if (ll != cur || c->fg_epoch == 0 || c->fg_epoch > (1u << 31) - need) {
+    unsigned& epoch = c->fg_epoch[tag + "fg_ll"];
+    if (ll != cur || epoch == 0 || epoch > (1u << 31) - need) {
       CK(cudaMemsetAsync(ll, 0, c->ws[tag + "fg_ll"].second, st));
-      c->fg_epoch = 1;
+      epoch = 1;
     }
-    sy.epoch0 = c->fg_epoch;
-    c->fg_epoch += need;
+    sy.epoch0 = epoch;
+    epoch += need;
     sy.red = ll;
     sy.xt = ll + 2 * 16 * static_cast<size_t>(sy.gstride);
     sy.xr = sy.xt + 2 * static_cast<size_t>(sy.gstride) * 2 * 32;
@@ -571,7 +578,7 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       // The grid did not fit co-resident (SMs taken by another context):
       // fall through to the cluster / split paths below.
       (void)cudaGetLastError();
-      c->fg_epoch -= need;
+      epoch -= need;
     } else {
       CK(le);
       c->launches++;
@@ -598,7 +605,9 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.x_s = static_cast<const T*>(kv.x_s);
     f.x0 = static_cast<const T*>(kv.x0);
     const int max_clusters = std::max(1, c->sm_count / fcG);
-    f.slot = static_cast<T*>(ws_get(c, "fc_slot", sizeof(T) * fcG * max_clusters *
+    // keyed by the stream tag: chunks on two streams may run concurrently and
+    // each CTA owns the slot at its blockIdx
+    f.slot = static_cast<T*>(ws_get(c, tag + "fc_slot", sizeof(T) * fcG * max_clusters *
                                                        fc_slot_elems<T>(K, n, fcG)));
     f.lambda0 = static_cast<const T*>(lambda0);
     f.lambda_out = static_cast<T*>(lambda_out);
@@ -647,7 +656,8 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.e = static_cast<const T*>(kv.e);
     f.x_s = static_cast<const T*>(kv.x_s);
     f.x0 = static_cast<const T*>(kv.x0);
-    f.slot = static_cast<T*>(ws_get(c, "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n, k->m)));
+    f.slot = static_cast<T*>(
+        ws_get(c, tag + "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n, k->m)));
     f.timing = env_int("B2P_PHASE_TIMING", 0)
                    ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
                    : nullptr;
@@ -796,6 +806,32 @@ void check_kind(int kind, int order) {
     throw invalid("build_preconditioner: unknown kind");
   if (kind == B2P_POLY_SPLIT && order < 1)
     throw invalid("build_poly_split: order must be >= 1, got " + std::to_string(order));
+}
+
+// Per-system status words for device-resident callers (b2p.h
+// b2p_solve_batched_device): {status, iterations, converged, aux} with aux =
+// the knot of a non-PD formation error, the PCG iteration of a breakdown /
+// non-finite error, else -1. Same decoding as resolve() / schur_msg() below.
+__global__ void k_pack_status(const SysOut* __restrict__ outs, const int* __restrict__ keys, int B,
+                              int32_t* __restrict__ st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  const int key = keys[i];
+  int32_t w[4];
+  if (key < 0x7f7f7f7f) {
+    const int b = key / 4, call = key % 4;
+    w[0] = B2P_RUNTIME_ERROR;
+    w[1] = 0;
+    w[2] = 0;
+    w[3] = b == 0 ? 0 : (call == 2 ? b : b - 1);
+  } else {
+    const SysOut o = outs[i];
+    w[0] = o.code;
+    w[1] = o.iterations;
+    w[2] = o.converged;
+    w[3] = o.code != kOk ? o.iteration : -1;
+  }
+  *reinterpret_cast<int4*>(st + 4 * static_cast<size_t>(i)) = make_int4(w[0], w[1], w[2], w[3]);
 }
 
 // Resolve per-system outcomes (host copies) into reports and a first error.
@@ -1566,7 +1602,13 @@ int b2p_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd
     else
       solve_device_impl<float>(c, kd, kv, batch, kind, order, cfg, lambda0_dev, lambda_out_dev,
                                dout, ek, nullptr, 0, st, true, "bd_");
-    (void)status_dev;
+    if (status_dev) {
+      if (reinterpret_cast<uintptr_t>(status_dev) % 16)
+        throw invalid("b2p_solve_batched_device: status_dev must be 16-byte aligned");
+      k_pack_status<<<(batch + 255) / 256, 256, 0, st>>>(dout, ek, batch, status_dev);
+      CK(cudaGetLastError());
+      c->launches++;
+    }
     if (reports) {
       std::vector<SysOut> outs(batch);
       std::vector<int> keys(batch);
@@ -1617,7 +1659,7 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
       cudaStream_t st = streams[sidx];
       const std::string tag = std::string("bh") + char('0' + sidx) + "_";
       void* in = ws_get(c, tag + "in", kkt_block_bytes(k, es, chunk));
-      const KktDev kv = upload_kkt(c, k, es, first, cnt, in, st);
+      const KktDev kv = upload_kkt(c, k, es, first, cnt, in, st, nullptr, 0, nullptr, false);
       char* dl0 = nullptr;
       if (lambda0) {
         dl0 = static_cast<char*>(ws_get(c, tag + "l0", es * D * chunk));

@@ -19,3 +19,22 @@ def test_adapter_reference_cases_on_gpu():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert "all checks passed" in out.stdout
+
+
+def test_dropin_compiles_against_the_reference_signatures():
+    """include/trajopt_dropin (the reference's Eigen-typed trajopt:: API) compiles
+    with an unmodified copy of sqp.cpp:171-176 and links libb2p.so."""
+    exe = b.build_dropin_test(force=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 0, out.stderr
+    assert "compiled and linked" in out.stdout
+
+
+@pytest.mark.gpu
+def test_dropin_reference_cases_on_gpu():
+    """The reference's KATs and the sqp.cpp:171-176 step through the drop-in on
+    the B200, checked against the CPU oracle (iterations equal, lambda 1e-10)."""
+    exe = b.build_dropin_test()
+    out = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "all checks passed" in out.stdout

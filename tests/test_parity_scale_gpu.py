@@ -1,0 +1,157 @@
+"""Parity at scale on the B200 (driver-visible: runs in `pytest -m gpu`).
+
+* the full 4096-system c4 bench batch (bench.py's seeds, symmetric stair,
+  eps 1e-8) and 1024 c4 systems at the NMPC tolerance eps 1e-4;
+* 256 c1 and 64 c2 systems for each of jacobi / stair / symmetric stair;
+every system's PCG iteration count and convergence flag equal to the oracle's
+(the reference restated, run on the same seeded inputs), lambda within 1e-10
+relative. Unpreconditioned CG (identity) is held to the documented policy
+(profiles/r02_identity_mismatches.json): the oracle's two
+reference variants themselves split on ~2 % of these systems.
+
+Also: the per-system device status words of b2p_solve_batched_device
+(status_dev) and the two-stream chunk pipeline of b2p_solve_batched with
+overlapping chunks (slot workspaces keyed per stream).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2309_08079_b200.types import PcgConfig, PrecondKind
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+KINDS = {"jacobi": PrecondKind.block_jacobi, "stair": PrecondKind.stair,
+         "symstair": PrecondKind.symmetric_stair}
+
+
+@pytest.fixture(scope="module")
+def api():
+    import paper_2309_08079_b200.api as a
+    a.require_device()
+    return a
+
+
+@pytest.fixture
+def env():
+    saved = dict(os.environ)
+    yield os.environ
+    os.environ.clear()
+    os.environ.update(saved)
+
+
+def _sweep(api, orc, seed0, B, N, n, m, kind, eps):
+    kb = api.random_kkt_batch(seed0, B, N, n, m)
+    cfg = PcgConfig(epsilon=eps)
+    lam, reps = api.solve_batched(kb, kind, 1, cfg)
+    _, lam_o, reps_o = orc.solve_batch(kb, kind, 1, cfg)
+    it_g = np.array([r.iterations for r in reps])
+    it_o = np.array([r.iterations for r in reps_o])
+    conv = np.array([r.converged for r in reps]) == np.array([r.converged for r in reps_o])
+    scale = np.maximum(1.0, np.abs(lam_o).max(axis=1))
+    rel = np.abs(lam - lam_o).max(axis=1) / scale
+    return it_g, it_o, conv, rel
+
+
+def test_c4_full_bench_batch_matches_oracle_per_system(api, orc):
+    """bench.py's c4 step input (seed 2309 + i, 4096 systems) — every system."""
+    it_g, it_o, conv, rel = _sweep(api, orc, 2309, 4096, 63, 14, 7,
+                                   PrecondKind.symmetric_stair, 1e-8)
+    bad = np.nonzero(it_g != it_o)[0]
+    assert bad.size == 0, f"{bad.size} systems differ, first {bad[:8]}"
+    assert conv.all()
+    assert rel.max() <= TOL64, rel.max()
+
+
+def test_c4_nmpc_tolerance_matches_oracle_per_system(api, orc):
+    it_g, it_o, conv, rel = _sweep(api, orc, 4000, 1024, 63, 14, 7,
+                                   PrecondKind.symmetric_stair, 1e-4)
+    assert np.array_equal(it_g, it_o) and conv.all()
+    assert rel.max() <= TOL64, rel.max()
+
+
+@pytest.mark.parametrize("kind", list(KINDS))
+@pytest.mark.parametrize("cfgname,seed0,B,N", [("c1", 100, 256, 31), ("c2", 300, 64, 127)])
+def test_every_preconditioner_per_system(api, orc, kind, cfgname, seed0, B, N):
+    it_g, it_o, conv, rel = _sweep(api, orc, seed0 + 10 * list(KINDS).index(kind), B, N, 14, 7,
+                                   KINDS[kind], 1e-8)
+    bad = np.nonzero(it_g != it_o)[0]
+    assert bad.size == 0, f"{cfgname} {kind}: {bad.size} systems differ, first {bad[:8]}"
+    assert conv.all()
+    assert rel.max() <= TOL64, rel.max()
+
+
+def test_identity_within_the_reference_variants_spread(api, orc):
+    """Unpreconditioned CG on random_kkt (kappa ~ 1e4, 80-95 steps): rounding
+    order decides the exit step. The B200 count must sit within one step of
+    the oracle's sequential or block-parallel variant on every system, match the
+    sequential count on >= 85 %, and its solution must meet the same exit test
+    (eta' < eps) — the reference's variants disagree with each other on the
+    same inputs (profiles/r02_identity_mismatches.json)."""
+    B = 256
+    kb = api.random_kkt_batch(800, B, 31, 14, 7)
+    cfg = PcgConfig(epsilon=1e-8)
+    lam, reps = api.solve_batched(kb, PrecondKind.identity, 1, cfg)
+    _, _, reps_s = orc.solve_batch(kb, PrecondKind.identity, 1, cfg)
+    _, _, reps_p = orc.solve_batch(kb, PrecondKind.identity, 1, PcgConfig(
+        epsilon=1e-8, variant=1, deterministic_reductions=True))
+    it_g = np.array([r.iterations for r in reps])
+    it_s = np.array([r.iterations for r in reps_s])
+    it_p = np.array([r.iterations for r in reps_p])
+    assert all(r.converged and r.exit_eta < 1e-8 for r in reps)
+    assert (np.minimum(np.abs(it_g - it_s), np.abs(it_g - it_p)) <= 1).all()
+    assert (it_g == it_s).mean() >= 0.85
+
+
+def test_status_dev_without_host_sync(api):
+    """b2p_solve_batched_device writes {status, iterations, converged, aux} per
+    system on the stream (b2p.h): a non-PD knot (aux = knot), a capped solve
+    (unconverged) and good systems, read back with a plain stream copy."""
+    import torch
+    from paper_2309_08079_b200.types import KKTSystem
+    B, N, n, m = 12, 63, 14, 7
+    kb = api.random_kkt_batch(777, B, N, n, m)
+    kb.Q[5][17] = -np.eye(n)  # system 5: Q at knot 17 not PD
+    dev = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in kb.arrays()]
+    kd = KKTSystem(N, n, m, *dev)
+    lam = torch.zeros((B, (N + 1) * n), dtype=torch.float64, device="cuda")
+    st = torch.full((B, 4), -7, dtype=torch.int32, device="cuda")
+    ctx = api.Context(0)
+    s = torch.cuda.Stream()
+    ctx.set_stream(s.cuda_stream)
+    api.solve_batched_device(kd, lam.data_ptr(), B, PrecondKind.symmetric_stair, 1,
+                             PcgConfig(epsilon=1e-8), ctx=ctx, status_ptr=st.data_ptr())
+    s.synchronize()
+    w = st.cpu().numpy()
+    assert w[5].tolist() == [2, 0, 0, 17]  # RUNTIME_ERROR, knot 17
+    good = [i for i in range(B) if i != 5]
+    assert (w[good, 0] == 0).all() and (w[good, 2] == 1).all() and (w[good, 3] == -1).all()
+    assert (w[good, 1] >= 8).all()
+    api.solve_batched_device(kd, lam.data_ptr(), B, PrecondKind.symmetric_stair, 1,
+                             PcgConfig(epsilon=1e-14, max_iter=3), ctx=ctx,
+                             status_ptr=st.data_ptr())
+    s.synchronize()
+    w = st.cpu().numpy()
+    assert (w[good, 0] == 0).all() and (w[good, 1] == 3).all() and (w[good, 2] == 0).all()
+    ctx.close()
+
+
+@pytest.mark.parametrize("kind", [PrecondKind.identity, PrecondKind.block_jacobi])
+def test_chunked_pipeline_with_overlapping_chunks(api, env, kind):
+    """b2p_solve_batched alternates chunks between two streams. With chunks
+    smaller than the SM count and long (weakly preconditioned, eps 1e-12)
+    solves, the chunks' kernels overlap on the device; results must equal the
+    single-chunk batch bitwise (per-stream slot workspaces, no shared staging)."""
+    B = 300
+    kb = api.random_kkt_batch(31337, B, 63, 14, 7)
+    cfg = PcgConfig(epsilon=1e-12)
+    lam1, rep1 = api.solve_batched(kb, kind, 1, cfg)
+    for chunk in ("37", "9"):  # > 8 systems per chunk: the same one-CTA kernel
+        env["B2P_BATCH_CHUNK"] = chunk
+        ctx = api.Context(0)
+        lam2, rep2 = api.solve_batched(kb, kind, 1, cfg, ctx=ctx)
+        ctx.close()
+        assert np.array_equal(lam1, lam2), chunk
+        assert [r.iterations for r in rep1] == [r.iterations for r in rep2]
