@@ -36,8 +36,12 @@ def _cmp(got, want, tol, eps):
     assert got.report.converged == want.report.converged
     assert got.report.iterations == want.report.iterations, (
         got.report.iterations, want.report.iterations, want.report.exit_eta / eps)
+    # Unpreconditioned CG (identity, 80-95 steps at kappa ~ 1e4) is the only regime
+    # here above 60 steps; there rounding order moves lambda itself by ~1e-6
+    # (profiles/r02_identity_mismatches.json). Every stair-family and Jacobi solve
+    # (<= 35 steps) is held to the plain bar.
     it = got.report.iterations
-    if it > 20:
+    if it > 60:
         tol = tol * (it / 10.0) ** 2
     err = rel_inf_error(got.lambda_, want.lambda_)
     assert err <= tol, err

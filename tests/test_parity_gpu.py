@@ -32,13 +32,12 @@ def _cmp(got, want, tol, eps):
         ratio = want.report.exit_eta / eps
         pytest.fail(f"iterations {got.report.iterations} != {want.report.iterations} "
                     f"(oracle eta'/eps = {ratio})")
-    # Rounding-order differences (GPU reduction trees vs the oracle's loops; the
-    # reference's Eigen packets differ from both) grow with the number of CG
-    # steps. The 1e-10 bar holds for the stair family (~10-14 steps on these
-    # instances). Weakly preconditioned solves (identity / Jacobi on random_kkt,
-    # kappa ~ 1e4, ~25-100 steps) are held to 1e-10 * (steps/10)^2.
+    # Unpreconditioned CG (identity, 80-95 steps at kappa ~ 1e4) is the only regime
+    # here above 60 steps; there rounding order moves lambda itself by ~1e-6
+    # (profiles/r02_identity_mismatches.json). Every stair-family and Jacobi solve
+    # (<= 35 steps) is held to the plain bar.
     it = got.report.iterations
-    if it > 20:
+    if it > 60:
         tol = tol * (it / 10.0) ** 2
     err = rel_inf_error(got.lambda_, want.lambda_)
     assert err <= tol, err
@@ -264,22 +263,22 @@ def test_one_cta_fused_kernel_every_preconditioner(api, orc, env, kind, K):
     from paper_2309_08079_b200.types import PcgVariant
     for i in (0, 5, 11):
         want = orc.solve(kb.system(i), kind, cfg=cfg)
-        if want.report.iterations <= 20:  # the stair family: exact parity
+        if kind != PrecondKind.identity:  # stair family and Jacobi: exact parity
             assert reps[i].iterations == want.report.iterations
         else:
-            # identity / Jacobi on kappa ~ 1e4: ~25-95 CG steps amplify rounding-order
-            # differences (loss of orthogonality); the reference's own two variants
-            # (sequential vs block-parallel tree reductions, pcg.cpp:55-129 / :157-362)
-            # already differ by one iteration on random_kkt_batch(7032) system 0. Accept
-            # either variant's count, or one step either side of it.
+            # identity on kappa ~ 1e4: 80-95 CG steps amplify rounding-order differences
+            # (loss of orthogonality); the reference's own two variants (sequential vs
+            # block-parallel tree reductions, pcg.cpp:55-129 / :157-362) split on ~9 %
+            # of such systems (profiles/r02_identity_mismatches.json). Accept either
+            # variant's count, or one step either side of it.
             par = orc.solve(kb.system(i), kind, cfg=PcgConfig(
                 epsilon=1e-8, variant=PcgVariant.block_parallel, deterministic_reductions=True))
             refs = (want.report.iterations, par.report.iterations)
             assert min(abs(reps[i].iterations - r) for r in refs) <= 1, (reps[i].iterations, refs)
-        if want.report.iterations <= 20:
+        if kind != PrecondKind.identity:
             assert rel_inf_error(lam[i], want.lambda_) <= TOL64
         else:
-            # identity / Jacobi: ~25-95 CG steps on kappa ~ 1e4 amplify rounding-order
+            # identity: 80-95 CG steps on kappa ~ 1e4 amplify rounding-order
             # differences in lambda itself; both solves must reach the same true
             # residual level (the reference's exit test is on r'r~, pcg.cpp:116)
             sch = orc.build_schur(kb.system(i))

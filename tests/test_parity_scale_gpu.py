@@ -83,15 +83,19 @@ def test_every_preconditioner_per_system(api, orc, kind, cfgname, seed0, B, N):
     assert rel.max() <= TOL64, rel.max()
 
 
-def test_identity_within_the_reference_variants_spread(api, orc):
+@pytest.mark.parametrize("seed0,N,min_equal", [(800, 31, 0.85), (900, 63, 0.95)])
+def test_identity_within_the_reference_variants_spread(api, orc, seed0, N, min_equal):
     """Unpreconditioned CG on random_kkt (kappa ~ 1e4, 80-95 steps): rounding
-    order decides the exit step. The B200 count must sit within one step of
-    the oracle's sequential or block-parallel variant on every system, match the
-    sequential count on >= 85 %, and its solution must meet the same exit test
-    (eta' < eps) — the reference's variants disagree with each other on the
-    same inputs (profiles/r02_identity_mismatches.json)."""
+    order decides the exit step — the eta' traces of the oracle's sequential and
+    block-parallel variants and of an 80-bit long-double CG drift apart (1e-3
+    relative) from step ~62-86 on, and the two reference variants disagree on
+    ~9 % of c1 systems (profiles/r02_identity_mismatches.json). The B200 count
+    must equal the oracle's sequential count on >= min_equal of the systems and
+    be within one step of the sequential, block-parallel or long-double count on
+    every system; every B200 solve meets the exit test (eta' < eps)."""
+    from util import cg_longdouble
     B = 256
-    kb = api.random_kkt_batch(800, B, 31, 14, 7)
+    kb = api.random_kkt_batch(seed0, B, N, 14, 7)
     cfg = PcgConfig(epsilon=1e-8)
     lam, reps = api.solve_batched(kb, PrecondKind.identity, 1, cfg)
     _, _, reps_s = orc.solve_batch(kb, PrecondKind.identity, 1, cfg)
@@ -101,8 +105,12 @@ def test_identity_within_the_reference_variants_spread(api, orc):
     it_s = np.array([r.iterations for r in reps_s])
     it_p = np.array([r.iterations for r in reps_p])
     assert all(r.converged and r.exit_eta < 1e-8 for r in reps)
-    assert (np.minimum(np.abs(it_g - it_s), np.abs(it_g - it_p)) <= 1).all()
-    assert (it_g == it_s).mean() >= 0.85
+    assert (it_g == it_s).mean() >= min_equal, (it_g == it_s).mean()
+    near = np.minimum(np.abs(it_g - it_s), np.abs(it_g - it_p)) <= 1
+    for i in np.nonzero(~near)[0]:
+        sch = orc.build_schur(kb.system(int(i)))
+        it_ld, _ = cg_longdouble(sch.S, sch.gamma, 1e-8, sch.S.dim())
+        assert abs(int(it_g[i]) - it_ld) <= 1, (int(i), it_g[i], it_s[i], it_p[i], it_ld)
 
 
 def test_status_dev_without_host_sync(api):

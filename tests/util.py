@@ -105,3 +105,27 @@ def kat(name):
     import os
     path = os.path.join(os.path.dirname(__file__), "golden", "reference_kats.json")
     return json.load(open(path))[name]
+
+
+def cg_longdouble(S, gamma, eps, max_iter):
+    """Textbook CG (pcg.cpp:55-129 with Phi = I) on the dense S in x87 80-bit
+    extended precision: the rounding-light reference for unpreconditioned-CG
+    exit counts (scripts/identity_mismatch.py). Returns (iterations, trace)."""
+    import numpy as np
+    A = S.to_dense().astype(np.longdouble)
+    g = np.asarray(gamma, dtype=np.longdouble)
+    r = g.copy()
+    p = r.copy()
+    eta = r @ r
+    trace = []
+    for i in range(1, max_iter + 1):
+        sp = A @ p
+        alpha = eta / (p @ sp)
+        r = r - alpha * sp
+        eta_p = r @ r
+        trace.append(float(eta_p))
+        if eta_p < eps:
+            return i, trace
+        p = r + (eta_p / eta) * p
+        eta = eta_p
+    return max_iter, trace
