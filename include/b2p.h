@@ -210,7 +210,10 @@ int b2p_solve_batched_device(b2p_ctx* ctx, int dtype, int batch, const b2p_kkt* 
                              b2p_solve_report* reports, int32_t* status_dev, b2p_error* err);
 
 /* K4: shard `batch` systems by contiguous batch index over `ndev` devices,
- * one host thread + context per device, no inter-GPU traffic. */
+ * one host thread + context per device, no inter-GPU traffic.
+ * The per-device contexts persist in a process-wide pool across calls (a
+ * device listed k times gets k contexts); every shard's context is ready
+ * before any device starts (host barrier). */
 int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
                             const b2p_kkt* kkt_batch, int kind, int order,
                             const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,

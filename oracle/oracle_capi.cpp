@@ -273,6 +273,23 @@ int orc_random_kkt(int family, uint64_t seed, int N, int n, int m, double diag_f
   return guard(err, [&] { write_kkt(gen(family, seed, N, n, m, diag_floor, coupling), out, 0); });
 }
 
+// Batch generator (the bench-pcg seeding rule, trajopt_cli.cpp:142-151): system
+// i = family(seed0 + i); `threads` host threads (0 = all).
+int orc_random_kkt_batch(int family, uint64_t seed0, int batch, int N, int n, int m,
+                         double diag_floor, double coupling, int threads, b2p_kkt_out* out,
+                         b2p_error* err) {
+  const int saved = hw_threads_override();
+  hw_threads_override() = threads;
+  const int rc = guard(err, [&] {
+    parallel_for(0, batch, [&](int i) {
+      write_kkt(gen(family, seed0 + static_cast<uint64_t>(i), N, n, m, diag_floor, coupling), out,
+                static_cast<std::size_t>(i));
+    });
+  });
+  hw_threads_override() = saved;
+  return rc;
+}
+
 int orc_build_schur(int dtype, const b2p_kkt* kkt, double* S, double* gamma, double* theta_inv,
                     b2p_error* err) {
   return guard(err, [&] {

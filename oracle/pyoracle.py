@@ -21,30 +21,53 @@ from paper_2309_08079_b200.types import (BlockTriMatrix, KKTSystem, PcgConfig, P
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
+# the labelled "-march=native" CPU row BASELINE.md §2 allows (bench.py only);
+# built on the machine that runs it (the GPU box's host CPU)
+LIB_NATIVE = os.path.join(HERE, "build", "liboracle_native.so")
 
 
-def build(force: bool = False) -> str:
-    """g++ -O3 -DNDEBUG (the reference's Release flags, proj/CMakeLists.txt:6-8)."""
+def build(force: bool = False, native: bool = False) -> str:
+    """g++ -O3 -DNDEBUG (the reference's Release flags, proj/CMakeLists.txt:6-8);
+    native=True adds -march=native into a separate library."""
+    out = LIB_NATIVE if native else LIB_PATH
     src = [os.path.join(HERE, "oracle_capi.cpp"), os.path.join(HERE, "trajopt_oracle.hpp")]
-    if (not force and os.path.exists(LIB_PATH)
-            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(s) for s in src)):
-        return LIB_PATH
-    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
-    cmd = ["g++", "-std=c++20", "-O3", "-DNDEBUG", "-fPIC", "-shared", "-pthread",
-           src[0], "-o", LIB_PATH]
-    subprocess.check_call(cmd)
-    return LIB_PATH
+    stamp = out + ".cpu"
+    same_cpu = not native or (os.path.exists(stamp) and open(stamp).read() == _cpu_signature())
+    if (not force and same_cpu and os.path.exists(out)
+            and os.path.getmtime(out) >= max(os.path.getmtime(s) for s in src)):
+        return out
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    tmp = out + f".{os.getpid()}.tmp"
+    cmd = ["g++", "-std=c++20", "-O3", "-DNDEBUG", "-fPIC", "-shared", "-pthread"]
+    cmd += ["-march=native"] if native else []
+    subprocess.check_call(cmd + [src[0], "-o", tmp])
+    os.replace(tmp, out)
+    if native:
+        open(stamp, "w").write(_cpu_signature())
+    return out
 
 
-_lib = None
+def _cpu_signature() -> str:
+    """Model name + ISA flags of this host: a -march=native build only runs here."""
+    try:
+        lines = open("/proc/cpuinfo").read().splitlines()
+    except OSError:
+        return "unknown"
+    keep = [ln for ln in lines if ln.startswith(("model name", "flags"))][:2]
+    return "\n".join(keep)
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
+_libs = {}
+
+
+def lib(native: bool = False):
+    if native not in _libs:
+        path = LIB_NATIVE if native else LIB_PATH
+        if native:
+            build(native=True)  # always for this host's CPU
+        elif not os.path.exists(path):
             build()
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         vp, i32, dbl, u64 = C.c_void_p, C.c_int, C.c_double, C.c_uint64
         E = C.POINTER(_abi.ErrorC)
         L.orc_set_threads.argtypes = [i32]
@@ -73,8 +96,10 @@ def lib():
                                       C.POINTER(_abi.SolveReportC), E]
         L.orc_solve_batch.restype = dbl
         L.orc_reconstruct_primal.argtypes = [i32, C.POINTER(_abi.KktC), vp, i32, vp, E]
-        _lib = L
-    return _lib
+        L.orc_random_kkt_batch.argtypes = [i32, u64, i32, i32, i32, i32, dbl, dbl, i32,
+                                           C.POINTER(_abi.KktOutC), E]
+        _libs[native] = L
+    return _libs[native]
 
 
 def _check(rc: int, err: _abi.ErrorC):
@@ -145,6 +170,18 @@ def random_kkt_scaled(seed, N, n, m, diag_floor, coupling) -> KKTSystem:  # :46-
 
 def random_trajectory_kkt(seed, N, n, m) -> KKTSystem:  # :51-80
     return _generate(2, seed, N, n, m)
+
+
+def random_kkt_batch(seed0: int, batch: int, N: int, n: int, m: int, family: int = 0,
+                     diag_floor: float = 0.1, coupling: float = 1.0, threads: int = 0,
+                     alloc=None) -> KKTSystem:
+    """System i = random_kkt(seed0 + i, ...) (the bench-pcg seeding rule)."""
+    kkt = KKTSystem.allocate(N, n, m, batch=batch, alloc=alloc)
+    out = _abi.KktOutC(N, n, m, 0, *[a.ctypes.data for a in kkt.arrays()])
+    err = _abi.ErrorC()
+    _check(lib().orc_random_kkt_batch(family, seed0, batch, N, n, m, diag_floor, coupling,
+                                      threads, C.byref(out), C.byref(err)), err)
+    return kkt
 
 
 def stack(kkts: list[KKTSystem]) -> KKTSystem:
@@ -328,7 +365,7 @@ def solve(kkt: KKTSystem, kind=PrecondKind.symmetric_stair, order: int = 1,
 
 def solve_batch(kkt_batch: KKTSystem, kind=PrecondKind.symmetric_stair, order: int = 1,
                 cfg: PcgConfig = None, threads: int = 0, dtype=np.float64,
-                want_lambda: bool = True):
+                want_lambda: bool = True, native: bool = False):
     """cmd_bench_pcg-style parallel_for over instances. Returns (seconds, lambda, reports)."""
     cfg = cfg or PcgConfig()
     kb = kkt_batch.astype(np.float64)
@@ -337,7 +374,7 @@ def solve_batch(kkt_batch: KKTSystem, kind=PrecondKind.symmetric_stair, order: i
     reps = (_abi.SolveReportC * B)()
     err = _abi.ErrorC()
     c = cfg.to_c()
-    secs = lib().orc_solve_batch(_dt(dtype), B, C.byref(kb.to_c()), int(kind), int(order),
+    secs = lib(native).orc_solve_batch(_dt(dtype), B, C.byref(kb.to_c()), int(kind), int(order),
                                  C.byref(c), int(threads), _ptr(lam), reps, C.byref(err))
     if secs < 0:
         _check(err.code, err)

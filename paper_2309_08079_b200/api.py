@@ -14,8 +14,8 @@ import numpy as np
 
 from . import _abi
 from ._lib import load
-from .types import (BlockTriMatrix, KKTSystem, PcgConfig, PcgResult, PcgVariant, Preconditioner,
-                    PrecondKind, SchurSystem, SolveReport, raise_for)
+from .types import (BatchReports, BlockTriMatrix, KKTSystem, PcgConfig, PcgResult, PcgVariant,
+                    Preconditioner, PrecondKind, SchurSystem, SolveReport, raise_for)
 
 _tls = threading.local()
 
@@ -386,7 +386,7 @@ def solve_batched(kkt_batch: KKTSystem, kind=PrecondKind.symmetric_stair, order:
     _check(load().b2p_solve_batched(ctx.handle, _dt(dt), B, C.byref(k.to_c()), int(kind),
                                     int(order), C.byref(c), _ptr(l0), _ptr(lam), reps,
                                     C.byref(err)), err)
-    return lam, [SolveReport.from_c(r) for r in reps]
+    return lam, BatchReports(reps)
 
 
 def solve_batched_device(kkt_dev: KKTSystem, lambda_out_ptr: int, batch: int,
@@ -407,7 +407,7 @@ def solve_batched_device(kkt_dev: KKTSystem, lambda_out_ptr: int, batch: int,
     _check(load().b2p_solve_batched_device(ctx.handle, _dt(dtype), batch, C.byref(kc),
                                            int(kind), int(order), C.byref(c), lambda0_ptr,
                                            lambda_out_ptr, reps, status_ptr, C.byref(err)), err)
-    return [SolveReport.from_c(r) for r in reps] if want_reports else None
+    return BatchReports(reps) if want_reports else None
 
 
 def reconstruct_primal(kkt: KKTSystem, lam, dtype=np.float64) -> np.ndarray:  # kkt.cpp:153-181
@@ -483,4 +483,4 @@ def solve_batched_multi(devices, kkt_batch: KKTSystem, kind=PrecondKind.symmetri
     _check(load().b2p_solve_batched_multi(devs, len(devices), _dt(dt), B, C.byref(k.to_c()),
                                           int(kind), int(order), C.byref(c), None, _ptr(lam),
                                           reps, C.byref(err)), err)
-    return lam, [SolveReport.from_c(r) for r in reps]
+    return lam, BatchReports(reps)

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <chrono>
 #include <climits>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1698,6 +1699,35 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
   });
 }
 
+}  // extern "C"
+namespace {
+// Persistent per-device contexts for b2p_solve_batched_multi: a call checks one
+// out per shard (creating it on first use) and returns it afterwards, so the
+// streams, events, pinned staging and workspaces survive across calls.
+std::mutex g_pool_mu;
+std::map<int, std::vector<b2p_ctx*>> g_pool;
+b2p_ctx* pool_checkout(int device, b2p_error* err, int* rc) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto& v = g_pool[device];
+    if (!v.empty()) {
+      b2p_ctx* c = v.back();
+      v.pop_back();
+      *rc = B2P_OK;
+      return c;
+    }
+  }
+  b2p_ctx* c = nullptr;
+  *rc = b2p_ctx_create(device, &c, err);
+  return c;
+}
+void pool_checkin(b2p_ctx* c) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool[c->device].push_back(c);
+}
+}  // namespace
+extern "C" {
+
 int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
                             const b2p_kkt* k, int kind, int order, const b2p_pcg_config* cfg,
                             const void* lambda0, void* lambda_out, b2p_solve_report* reports,
@@ -1713,13 +1743,21 @@ int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
     std::vector<b2p_error> errs(ndev);
     std::vector<std::thread> th;
     const int per = (batch + ndev - 1) / ndev;
-    for (int g = 0; g < ndev; ++g) {
+    const int active = std::min(ndev, (batch + per - 1) / per);
+    // host barrier: every shard's context is ready before any device starts
+    std::mutex bm;
+    std::condition_variable bcv;
+    int arrived = 0;
+    for (int g = 0; g < active; ++g) {
       th.emplace_back([&, g] {
         const int first = g * per, cnt = std::min(per, batch - first);
-        if (cnt <= 0) return;
-        b2p_ctx* cx = nullptr;
-        rc[g] = b2p_ctx_create(devices[g], &cx, &errs[g]);
-        if (rc[g] != B2P_OK) return;
+        b2p_ctx* cx = pool_checkout(devices[g], &errs[g], &rc[g]);
+        {
+          std::unique_lock<std::mutex> lk(bm);
+          if (++arrived == active) bcv.notify_all();
+          else bcv.wait(lk, [&] { return arrived == active; });
+        }
+        if (rc[g] != B2P_OK || !cx) return;
         // contiguous batch-index shard
         const size_t nn = size_t(n) * n, Kz = K, Nz = N;
         auto off = [&](const void* p, size_t per_sys) {
@@ -1739,12 +1777,12 @@ int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
         void* lo = static_cast<char*>(lambda_out) + es * D * first;
         rc[g] = b2p_solve_batched(cx, dtype, cnt, &s, kind, order, cfg, l0, lo,
                                   reports ? reports + first : nullptr, &errs[g]);
-        if (rc[g] != B2P_OK) errs[g].system += first;
-        b2p_ctx_destroy(cx);
+        if (rc[g] != B2P_OK && errs[g].system >= 0) errs[g].system += first;
+        pool_checkin(cx);
       });
     }
     for (auto& t : th) t.join();
-    for (int g = 0; g < ndev; ++g)
+    for (int g = 0; g < active; ++g)
       if (rc[g] != B2P_OK) {
         Fail f{rc[g], errs[g].message};
         f.knot = errs[g].knot;

@@ -152,6 +152,79 @@ __device__ __forceinline__ void tm_ld_row14(unsigned taddr, double (&v)[14]) {
 #pragma unroll
   for (int j = 0; j < 14; ++j) v[j] = __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j]));
 }
+// (o0, o1) = (row t0 . x, row t1 . x) for two 14-double TMEM rows of the calling
+// thread's lane against one 16-byte aligned shared vector: each broadcast x pair
+// serves both rows. Loaded in two column halves (8 + 6 doubles) to bound the
+// live registers; per row the same two-accumulator order as dot_rm.
+__device__ __forceinline__ void tm_dot2_row14(unsigned t0, unsigned t1, const double* x,
+                                              double& o0, double& o1) {
+  double a0 = 0.0, c0 = 0.0, a1 = 0.0, c1 = 0.0;
+  {
+    unsigned u[16], w[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];\n"
+        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+          "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+          "=r"(u[14]), "=r"(u[15])
+        : "r"(t0));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];\n"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+          "=r"(w[14]), "=r"(w[15])
+        : "r"(t1));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]),
+                   "+r"(u[6]), "+r"(u[7]), "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]),
+                   "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15]), "+r"(w[0]), "+r"(w[1]),
+                   "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
+                   "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]),
+                   "+r"(w[14]), "+r"(w[15]));
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(x + j);
+      a0 += __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j])) * v.x;
+      c0 += __hiloint2double(static_cast<int>(u[2 * j + 3]), static_cast<int>(u[2 * j + 2])) * v.y;
+      a1 += __hiloint2double(static_cast<int>(w[2 * j + 1]), static_cast<int>(w[2 * j])) * v.x;
+      c1 += __hiloint2double(static_cast<int>(w[2 * j + 3]), static_cast<int>(w[2 * j + 2])) * v.y;
+    }
+  }
+  {
+    unsigned u[12], w[12];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),
+                   "=r"(u[6]), "=r"(u[7])
+                 : "r"(t0 + 16));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11])
+                 : "r"(t0 + 24));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                   "=r"(w[6]), "=r"(w[7])
+                 : "r"(t1 + 16));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11])
+                 : "r"(t1 + 24));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+                 : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]),
+                   "+r"(u[6]), "+r"(u[7]), "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]),
+                   "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]),
+                   "+r"(w[6]), "+r"(w[7]), "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]));
+#pragma unroll
+    for (int j = 0; j < 6; j += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(x + 8 + j);
+      a0 += __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j])) * v.x;
+      c0 += __hiloint2double(static_cast<int>(u[2 * j + 3]), static_cast<int>(u[2 * j + 2])) * v.y;
+      a1 += __hiloint2double(static_cast<int>(w[2 * j + 1]), static_cast<int>(w[2 * j])) * v.x;
+      c1 += __hiloint2double(static_cast<int>(w[2 * j + 3]), static_cast<int>(w[2 * j + 2])) * v.y;
+    }
+  }
+  o0 = a0 + c0;
+  o1 = a1 + c1;
+}
+
 // sum_j m[j] x[j] (m in registers, x a 16-byte aligned shared vector), two partial sums
 template <int NB>
 __device__ __forceinline__ double dot_rm(const double (&m)[NB], const double* x) {
@@ -165,11 +238,17 @@ __device__ __forceinline__ double dot_rm(const double (&m)[NB], const double* x)
   return a + c;
 }
 
-// per-CTA slot stride in elements, padded to 16 bytes (the TMA source must be aligned)
+// Block stride (elements) of L in the slot and in shared memory: n*n padded to
+// 8 mod 32 doubles, so the four quarter-warps of a PCG warp (consecutive block
+// rows) read their column-product operands from disjoint banks (n = 14: 200).
+__host__ __device__ constexpr int fused_ls(int n) { return n * n + ((8 - (n * n) % 32) + 32) % 32; }
+
+// per-CTA slot stride in elements, padded to 16 bytes (the TMA source must be aligned):
+// L [K][LS] | D [K][n n] | theta^-1 [K][n n] | gamma [K][n] | R^-1 [K][m m]
 template <class T>
 __host__ __device__ inline size_t fused_slot_stride(int K, int n, int m) {
-  const size_t e = static_cast<size_t>(2) * K * n * n + static_cast<size_t>(K) * n +
-                   static_cast<size_t>(K) * m * m;
+  const size_t e = static_cast<size_t>(K) * fused_ls(n) + static_cast<size_t>(2) * K * n * n +
+                   static_cast<size_t>(K) * n + static_cast<size_t>(K) * m * m;
   const size_t a = 16 / sizeof(T);
   return (e + a - 1) / a * a;
 }
@@ -188,12 +267,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   const int h = tid >> 4;         // half-warp index = owned block row (first)
   const bool lact = l < NB;
   T* smem = reinterpret_cast<T*>(smem_raw);
-  // PCG layout
-  // PCG layout starts after the formation's Q region: while system s runs its
-  // PCG, the Q_k and q_k of the CTA's next system are TMA-prefetched into
-  // [0, K*NN) and the q region (both untouched by the PCG phase)
-  T* sL = smem + static_cast<size_t>(K) * NN;  // [K][NB][NB] (column products)
-  T* sp = sL + static_cast<size_t>(K) * NN;  // [K][NB]
+  // PCG layout. [0, K*NN): D staged from the slot at the start of the phase
+  // (slot -> shared -> TMEM), then the next system's Q_k, TMA-prefetched for
+  // its formation while this system's PCG runs (as are its q_k, into the q
+  // region past `red`); sL: the L blocks at the padded stride LS.
+  constexpr int LS = fused_ls(NB);
+  T* sD = smem;                                 // [K][NB][NB]
+  T* sL = smem + static_cast<size_t>(K) * NN;   // [K][LS]    (column products)
+  T* sp = sL + static_cast<size_t>(K) * LS;     // [K][NB]
   T* st = sp + K * NB;
   T* su = st + K * NB;
   T* red = su + K * NB;                  // [64]
@@ -226,11 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   const unsigned tbase = s_taddr + ((32u * ((tid >> 5) & 3)) << 16) + 128u * (tid >> 7);
   auto colD = [&](int r) { return tbase + 32u * r; };
   auto colL = [&](int r) { return tbase + 64u + 32u * r; };
-  // CTA-private global slot (L2 resident)
-  // CTA-private slot (L2 resident): L (TMA-staged for the column products),
-  // theta^-1, gamma, R^-1; D never leaves the SM (formation registers -> TMEM)
+  // CTA-private slot (L2 resident): L and D (TMA-staged for the PCG phase),
+  // theta^-1, gamma, R^-1
   T* gL = p.slot + static_cast<size_t>(blockIdx.x) * fused_slot_stride<T>(K, NB, MB);
-  T* gT = gL + static_cast<size_t>(K) * NN;
+  T* gD = gL + static_cast<size_t>(K) * LS;
+  T* gT = gD + static_cast<size_t>(K) * NN;
   T* gG = gT + static_cast<size_t>(K) * NN;  // gamma [K][NB]
   T* gR = gG + static_cast<size_t>(K) * NB;  // R_k^-1 [N][MB][MB]
 
@@ -443,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
           tW[i * LD + l] = x[i];
-          if (wr) gL[static_cast<size_t>(b) * nn + i * NB + l] = -x[i];
+          if (wr) gL[static_cast<size_t>(b) * LS + i * NB + l] = -x[i];
           if (wr && p.form_only)  // S.left(b) = phi (schur.cpp:74)
             p.S_out[(static_cast<size_t>(sys) * K + b) * 3 * nn + i * NB + l] = -x[i];
         }
@@ -451,16 +532,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int q = 0; q < MB; ++q) tBR[l * LDM + q] = br[q];
       }
       __syncwarp();
-      {  // row l of L_b = -AQ -> TMEM (the row products of the PCG phase)
-        T lrow[NB];
+      if (wr && lact && p.form_only) {  // S.right(b-1) = phi' (schur.cpp:74)
 #pragma unroll
-        for (int j = 0; j < NB; ++j) lrow[j] = -tW[lr * LD + j];
-        tm_st_row14(colL(r), lrow);
-        if (wr && lact && p.form_only) {  // S.right(b-1) = phi' (schur.cpp:74)
-#pragma unroll
-          for (int j = 0; j < NB; ++j)
-            p.S_out[((static_cast<size_t>(sys) * K + b - 1) * 3 + 2) * nn + j * NB + l] = lrow[j];
-        }
+        for (int j = 0; j < NB; ++j)
+          p.S_out[((static_cast<size_t>(sys) * K + b - 1) * 3 + 2) * nn + j * NB + l] =
+              -tW[lr * LD + j];
       }
       // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
 #pragma unroll
@@ -487,15 +563,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         }
       }
       hw_symmetrize_col<T, NB, LD, true>(tW, l, x);  // theta (schur.cpp:67)
-      {  // row l of D_b = theta (row 0: Q_0^-1, schur.cpp:53) -> TMEM
-        T drow[NB];
+      if ((wr || b0 == 0) && lact) {
+        // D_b = theta (row 0: Q_0^-1, schur.cpp:53) -> the slot, stored as columns
+        // (both are bitwise symmetric, so column l = row l): the PCG phase stages
+        // it into TMEM in its own row mapping
+        const int bd = b0 == 0 ? 0 : b;
 #pragma unroll
-        for (int i = 0; i < NB; ++i) drow[i] = (b0 == 0) ? sQi[lr * NB + i] : x[i];
-        tm_st_row14(colD(r), drow);
-        if (wr && lact && p.form_only) {  // S.diag(b) = theta (schur.cpp:73)
-#pragma unroll
-          for (int i = 0; i < NB; ++i)
-            p.S_out[((static_cast<size_t>(sys) * K + b) * 3 + 1) * nn + i * NB + l] = drow[i];
+        for (int i = 0; i < NB; ++i) {
+          const T d = (b0 == 0) ? sQi[lr * NB + i] : x[i];
+          gD[static_cast<size_t>(bd) * nn + i * NB + l] = d;
+          if (p.form_only)  // S.diag(b) = theta (schur.cpp:73)
+            p.S_out[((static_cast<size_t>(sys) * K + bd) * 3 + 1) * nn + i * NB + l] = d;
         }
       }
       // theta^-1 (schur.cpp:75): x holds row l of the symmetric theta
@@ -515,7 +593,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         }
       }
     }
-    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    // F2's global writes (L, D, theta^-1, gamma) are read back by the async
+    // proxy (TMA) below: order them before the barrier
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
     if (tm) tm[2] = gtimer();
     if (l == 0 && fkey != 0x7fffffff) atomicMin(&s_err, fkey);
     __syncthreads();
@@ -534,17 +614,81 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     if (p.form_only) continue;  // build_schur only
 
     // ================================================================ P
-    // stage L, D (contiguous in the slot and in shared memory) with one TMA
-    // bulk copy completed on an mbarrier; then prefetch the next system's
-    // KKT inputs into L2 so its formation phase does not start on cold HBM.
+    // PCG mapping: warp w owns block rows 4w..4w+3, one per quarter-warp; lane
+    // i < 7 of a quarter-warp owns scalar rows i and i + 7 of its block, so
+    // every broadcast operand vector serves two output rows. D_b and L_b rows
+    // live in TMEM, L (for the column products R_b = L_{b+1}') in shared memory,
+    // theta_b^-1 rows in registers.
+    const int pq = lane >> 3;  // quarter-warp
+    const int pi = lane & 7;   // row pair (pi, pi + 7); lane 7 of each quarter idles
+    const int pb = 4 * (tid >> 5) + pq;
+    const bool pact = pi < 7 && pb < K;
+    const int pbc = pb < K ? pb : K - 1;            // clamped block row
+    const int pbl = pbc > 0 ? pbc - 1 : 0;          // neighbours, clamped into [0, K):
+    const int pbn = pbc + 1 < K ? pbc + 1 : K - 1;  // edge products are discarded
+    const int pr = pi < 7 ? pi : 6;                 // clamped row (idle lanes)
     {
-      const unsigned bytes = static_cast<unsigned>(sizeof(T) * K * NN);
-      if (tid == 0) tma_load_1d(sL, gL, bytes, mbar_addr);
+      // stage D and L from the slot (one TMA bulk copy each), then every thread
+      // moves its own rows into its TMEM lane
+      const unsigned bd = static_cast<unsigned>(sizeof(T) * K * NN);
+      const unsigned bl = static_cast<unsigned>(sizeof(T) * K * LS);
+      if (tid == 0) {
+        asm volatile("fence.proxy.async;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
+                     "r"(bd + bl)
+                     : "memory");
+        tma_copy_1d(sD, gD, bd, mbar_addr);
+        tma_copy_1d(sL, gL, bl, mbar_addr);
+      }
+    }
+    T ti[2][NB];
+    T lam[2], rr[2], rt[2], pp[2], spv[2], best[2], gam[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int row = pr + 7 * c;
+      // theta^-1 row, stored transposed by F2 (bitwise symmetric)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) ti[c][j] = __ldcg(gT + static_cast<size_t>(pbc) * NN + j * NB + row);
+      gam[c] = __ldcg(gG + pbc * NB + row);
+      lam[c] = (pact && p.lambda0) ? p.lambda0[static_cast<size_t>(sys) * K * NB + pbc * NB + row]
+                                   : T(0);
+    }
+    mbar_wait(mbar_addr, mbar_phase);
+    {
+      T m[NB];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const T* Dr = sD + static_cast<size_t>(pbc) * NN + (pr + 7 * c) * NB;
+#pragma unroll
+        for (int j = 0; j < NB; j += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(Dr + j);
+          m[j] = v.x;
+          m[j + 1] = v.y;
+        }
+        tm_st_row14(colD(c), m);
+        const T* Lr = sL + static_cast<size_t>(pbc) * LS + (pr + 7 * c) * NB;
+#pragma unroll
+        for (int j = 0; j < NB; j += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(Lr + j);
+          m[j] = v.x;
+          m[j + 1] = v.y;
+        }
+        tm_st_row14(colL(c), m);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      if (pact) sp[pbc * NB + pi + 7 * c] = lam[c];
+    __syncthreads();  // sD consumed: the next system's Q may land in [0, K*NN)
+    if (tm) tm[3] = gtimer();
+    {
       const int nsys = sys + gridDim.x;
       if (nsys < p.B) {  // next system's Q_k, q_k straight into the formation's regions
         if (tid == 0) {
           const unsigned bq = static_cast<unsigned>(sizeof(T) * K * nn);
           const unsigned bv = static_cast<unsigned>(sizeof(T) * K * NB);
+          asm volatile("fence.proxy.async;\n" ::: "memory");
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar2_addr),
                        "r"(bq + bv)
                        : "memory");
@@ -570,139 +714,80 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
                        : "memory");
       }
     }
-    if (tm) tm[3] = gtimer();
-    T ti[R][NB];
-    T lam[R], rr[R], rt[R], pp[R], spv[R], best[R], gam[R];
-    int bb[R];
-    bool act[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      bb[r] = h + r * kHalfWarps;
-      act[r] = bb[r] < K && lact;
-      const int b = bb[r] < K ? bb[r] : K - 1;
-      // theta^-1 row l, stored transposed by F2 (coalesced both ways)
-#pragma unroll
-      for (int i = 0; i < NB; ++i) ti[r][i] = __ldcg(gT + static_cast<size_t>(b) * NN + i * NB + (lact ? l : 0));
-      gam[r] = __ldcg(gG + b * NB + (lact ? l : 0));
-      lam[r] = (act[r] && p.lambda0) ? p.lambda0[static_cast<size_t>(sys) * K * NB + b * NB + l]
-                                     : T(0);
-      if (act[r]) sp[b * NB + l] = lam[r];
-    }
-    mbar_wait(mbar_addr, mbar_phase);
-    __syncthreads();
 
-    int bc[R];  // clamped block row per owned row
-    int bl[R], bn[R];  // its neighbour rows, clamped into [0, K): the edge rows'
-                       // products are discarded, but must not read the next
-                       // shared-memory array while other threads write it
+    // y_c = ((D x_b + L x_{b-1}) + R x_{b+1}) for the thread's rows pi, pi + 7,
+    // R_b = L_{b+1}' (block_tri.cpp:82-92). Out-of-range neighbours are computed
+    // on in-bounds shared memory and discarded by the selects.
+    auto Srows = [&](const T* x, T (&y)[2]) {
+      T sd[2], sl[2], sr[2];
+      tm_dot2_row14(colD(0), colD(1), x + pbc * NB, sd[0], sd[1]);  // D_b rows (TMEM)
+      tm_dot2_row14(colL(0), colL(1), x + pbl * NB, sl[0], sl[1]);  // L_b rows (TMEM)
+      dots_col2<T, NB, LS>(sL + static_cast<size_t>(pbn) * LS + pr, x + pbn * NB, sr);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      bc[r] = bb[r] < K ? bb[r] : K - 1;
-      bl[r] = bc[r] > 0 ? bc[r] - 1 : 0;
-      bn[r] = bc[r] + 1 < K ? bc[r] + 1 : K - 1;
-    }
-    // y_r = ((D x_b + L x_{b-1}) + R x_{b+1}) for the R owned rows, R_b = L_{b+1}'
-    // (block_tri.cpp:82-92). Out-of-range neighbours are computed on
-    // in-bounds shared memory and discarded by the selects.
-    auto Srows = [&](const T* x, T (&y)[R]) {
-      const T *Mp[R], *Xp[R];
-      T sd[R], sl[R], sr[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {  // D_b and L_b rows from TMEM
-        T m[NB];
-        tm_ld_row14(colD(r), m);
-        sd[r] = dot_rm<NB>(m, x + bc[r] * NB);
-        tm_ld_row14(colL(r), m);
-        sl[r] = dot_rm<NB>(m, x + bl[r] * NB);
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        Mp[r] = sL + static_cast<size_t>(bn[r]) * NN + l;
-        Xp[r] = x + bn[r] * NB;
-      }
-      dots_col<T, NB, R>(Mp, Xp, sr);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        T out = sd[r];
-        if (bc[r] > 0) out += sl[r];
-        if (bc[r] + 1 < K) out += sr[r];
-        y[r] = out;
+      for (int c = 0; c < 2; ++c) {
+        T out = sd[c];
+        if (pbc > 0) out += sl[c];
+        if (pbc + 1 < K) out += sr[c];
+        y[c] = out;
       }
     };
 
     // r = gamma - S lambda0 (pcg.cpp:62)
+    __syncthreads();
     {
-      T sl0[R];
+      T sl0[2];
       if (p.lambda0) Srows(sp, sl0);
 #pragma unroll
-      for (int r = 0; r < R; ++r) rr[r] = gam[r] - (p.lambda0 ? sl0[r] : T(0));
+      for (int c = 0; c < 2; ++c) rr[c] = gam[c] - (p.lambda0 ? sl0[c] : T(0));
     }
     // r~ = Phi^-1 r, for every kind
+    const bool corr_row = (p.kind == kSymStair) || (pbc & 1);
     auto precondition = [&]() {
       if (p.kind == kIdentity) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) rt[r] = rr[r];
+        for (int c = 0; c < 2; ++c) rt[c] = rr[c];
         return;
       }
-      T tv[R];
-      const T* Vp[R];
+      T tv[2];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (act[r]) su[bb[r] * NB + l] = rr[r];
-        Vp[r] = su + bc[r] * NB;
-      }
+      for (int c = 0; c < 2; ++c)
+        if (pact) su[pbc * NB + pi + 7 * c] = rr[c];
       __syncwarp();
-      dots_reg<T, NB, R>(ti, Vp, tv);  // t = theta^-1 r
+      dots_reg2<T, NB>(ti, su + pbc * NB, tv);  // t = theta^-1 r
       if (p.kind == kJacobi) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) rt[r] = tv[r];
+        for (int c = 0; c < 2; ++c) rt[c] = tv[c];
         return;
       }
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (act[r]) st[bb[r] * NB + l] = tv[r];
+      for (int c = 0; c < 2; ++c)
+        if (pact) st[pbc * NB + pi + 7 * c] = tv[c];
       __syncthreads();
       // u = r - L_b t_{b-1} - R_b t_{b+1}
-      T sl[R], sr[R];
-      {
-        const T *Mp[R], *Xp[R];
+      T sl[2], sr[2];
+      tm_dot2_row14(colL(0), colL(1), st + pbl * NB, sl[0], sl[1]);
+      dots_col2<T, NB, LS>(sL + static_cast<size_t>(pbn) * LS + pr, st + pbn * NB, sr);
+      __syncwarp();  // every lane has read its block's r from su
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          T m[NB];
-          tm_ld_row14(colL(r), m);
-          sl[r] = dot_rm<NB>(m, st + bl[r] * NB);
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          Mp[r] = sL + static_cast<size_t>(bn[r]) * NN + l;
-          Xp[r] = st + bn[r] * NB;
-        }
-        dots_col<T, NB, R>(Mp, Xp, sr);
+      for (int c = 0; c < 2; ++c) {
+        T v = rr[c];
+        if (pbc > 0) v -= sl[c];
+        if (pbc + 1 < K) v -= sr[c];
+        if (pact) su[pbc * NB + pi + 7 * c] = v;
       }
       __syncwarp();
+      T uv[2];
+      dots_reg2<T, NB>(ti, su + pbc * NB, uv);  // theta^-1 u
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        T v = rr[r];
-        if (bc[r] > 0) v -= sl[r];
-        if (bc[r] + 1 < K) v -= sr[r];
-        if (act[r]) su[bb[r] * NB + l] = v;
-      }
-      __syncwarp();
-      T uv[R];
-      dots_reg<T, NB, R>(ti, Vp, uv);  // theta^-1 u
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const bool corr = (p.kind == kSymStair) || (bc[r] & 1);
-        rt[r] = corr ? uv[r] : tv[r];
-      }
+      for (int c = 0; c < 2; ++c) rt[c] = corr_row ? uv[c] : tv[c];
     };
     precondition();
     T eta_part = T(0);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      pp[r] = rt[r];
-      if (act[r]) eta_part += rr[r] * rt[r];
-      best[r] = lam[r];
+    for (int c = 0; c < 2; ++c) {
+      pp[c] = rt[c];
+      if (pact) eta_part += rr[c] * rt[c];
+      best[c] = lam[c];
     }
     T eta = block_reduce(eta_part, red);
 
@@ -717,15 +802,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       converged = 1;
     } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (act[r]) sp[bb[r] * NB + l] = pp[r];
+      for (int c = 0; c < 2; ++c)
+        if (pact) sp[pbc * NB + pi + 7 * c] = pp[c];
       __syncthreads();
       for (int it = 1; it <= p.max_iter; ++it) {
         T up = T(0);
         Srows(sp, spv);
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (act[r]) up += pp[r] * spv[r];
+        for (int c = 0; c < 2; ++c)
+          if (pact) up += pp[c] * spv[c];
         const T ups = block_reduce(up, red + 32);  // buffer B
         if (!is_finite(ups)) {
           code = kRuntime;
@@ -742,15 +827,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         }
         const T alpha = eta / ups;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          rr[r] -= alpha * spv[r];
-          lam[r] += alpha * pp[r];
+        for (int c = 0; c < 2; ++c) {
+          rr[c] -= alpha * spv[c];
+          lam[c] += alpha * pp[c];
         }
         precondition();
         T ep = T(0);
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (act[r]) ep += rr[r] * rt[r];
+        for (int c = 0; c < 2; ++c)
+          if (pact) ep += rr[c] * rt[c];
         const T eta_p = block_reduce(ep, red);
         if (!is_finite(eta_p)) {
           code = kRuntime;
@@ -762,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         if (eta_p < best_eta) {
           best_eta = eta_p;
 #pragma unroll
-          for (int r = 0; r < R; ++r) best[r] = lam[r];
+          for (int c = 0; c < 2; ++c) best[c] = lam[c];
         }
         iterations = it;
         exit_eta = static_cast<double>(eta_p);
@@ -773,9 +858,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         if (it == p.max_iter) break;
         const T beta = eta_p / eta;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          pp[r] = rt[r] + beta * pp[r];
-          if (act[r]) sp[bb[r] * NB + l] = pp[r];
+        for (int c = 0; c < 2; ++c) {
+          pp[c] = rt[c] + beta * pp[c];
+          if (pact) sp[pbc * NB + pi + 7 * c] = pp[c];
         }
         eta = eta_p;
         __syncthreads();
@@ -783,10 +868,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     }
     if (code == kOk) {
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (act[r])
-          p.lambda_out[static_cast<size_t>(sys) * K * NB + bb[r] * NB + l] =
-              converged ? lam[r] : best[r];
+      for (int c = 0; c < 2; ++c)
+        if (pact)
+          p.lambda_out[static_cast<size_t>(sys) * K * NB + pbc * NB + pi + 7 * c] =
+              converged ? lam[c] : best[c];
     }
     if (tid == 0) {
       SysOut o;
@@ -814,7 +899,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 template <class T, int NB, int MB>
 size_t fused_smem_bytes(int K) {
   using FL = FLayout<T, NB, MB>;
-  const size_t pcg = sizeof(T) * (static_cast<size_t>(2) * K * NB * NB + 3 * K * NB + 64);
+  const size_t pcg =
+      sizeof(T) * (static_cast<size_t>(K) * (NB * NB + fused_ls(NB)) + 3 * K * NB + 64);
   const size_t form = sizeof(T) * static_cast<size_t>(FL::total(K));
   return std::max(pcg, form);
 }

@@ -181,6 +181,40 @@ __device__ __forceinline__ void dots_col(const T* (&Mc)[R], const T* (&x)[R], T 
 #pragma unroll
   for (int r = 0; r < R; ++r) out[r] = a[r] + c[r];
 }
+// Two rows (pr, pr + NB/2) of one block per thread (the one-CTA kernel's PCG
+// mapping): out[c] = sum_j Mc[j*NB + c*NB/2] * x[j] — columns pr and pr + NB/2
+// of a row-major block (Mc = block + pr), one broadcast x serving both; same
+// two-accumulator order as dots_col.
+template <class T, int NB, int LS>
+__device__ __forceinline__ void dots_col2(const T* Mc, const T* x, T (&out)[2]) {
+  constexpr int H = NB / 2;
+  T a0 = T(0), c0 = T(0), a1 = T(0), c1 = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+    const double2 v2 = *reinterpret_cast<const double2*>(x + j);
+    a0 += Mc[j * NB] * v2.x;
+    a1 += Mc[j * NB + H] * v2.x;
+    c0 += Mc[(j + 1) * NB] * v2.y;
+    c1 += Mc[(j + 1) * NB + H] * v2.y;
+  }
+  out[0] = a0 + c0;
+  out[1] = a1 + c1;
+}
+// out[c] = ti[c] . v for two register rows against one shared vector
+template <class T, int NB>
+__device__ __forceinline__ void dots_reg2(const T (&ti)[2][NB], const T* v, T (&out)[2]) {
+  T a0 = T(0), c0 = T(0), a1 = T(0), c1 = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+    const double2 v2 = *reinterpret_cast<const double2*>(v + j);
+    a0 += ti[0][j] * v2.x;
+    c0 += ti[0][j + 1] * v2.y;
+    a1 += ti[1][j] * v2.x;
+    c1 += ti[1][j + 1] * v2.y;
+  }
+  out[0] = a0 + c0;
+  out[1] = a1 + c1;
+}
 // out[r] = ti[r] . v[r]  (theta^-1 row held in registers)
 template <class T, int NB, int R>
 __device__ __forceinline__ void dots_reg(const T (&ti)[R][NB], const T* (&v)[R], T (&out)[R]) {

@@ -114,6 +114,43 @@ class SolveReport:  # pcg.hpp:31-38
                            float(rep.wall_time), float(rep.max_residual_drift))
 
 
+class BatchReports:
+    """Per-system SolveReports of a batched call, decoded lazily from the C
+    array (a 4096-system batch would otherwise spend milliseconds building
+    Python objects). Indexing / iteration yields SolveReport; the fields are
+    also available whole as numpy arrays (.iterations, .converged, ...)."""
+
+    def __init__(self, arr):
+        self._c = arr
+        self._np = np.ctypeslib.as_array(arr)
+
+    def __len__(self) -> int:
+        return len(self._c)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        return SolveReport.from_c(self._c[i])
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+    def field(self, name: str) -> np.ndarray:
+        return self._np[name].copy()
+
+    @property
+    def iterations(self) -> np.ndarray:
+        return self.field("iterations")
+
+    @property
+    def converged(self) -> np.ndarray:
+        return self.field("converged").astype(bool)
+
+    @property
+    def exit_eta(self) -> np.ndarray:
+        return self.field("exit_eta")
+
+
 @dataclass
 class PcgResult:  # pcg.hpp:40-43
     lambda_: np.ndarray

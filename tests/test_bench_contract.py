@@ -39,16 +39,37 @@ def test_b200_arm_contract():
     assert d["unit"] == "solves/s" and d["higher_is_better"] is True and d["scaling"] == "weak"
     assert d["gpu_launches"] >= d["steps"]
     r = d["roofline"]
-    assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] < 1 and r["peak"] > 0
-    assert r["fp64"]["unit"] == "TFLOP/s" and 0 < r["fp64"]["frac"] < 1
+    # the binding roof: FP64 FMA work; the HBM view beside it
+    assert r["bound"] == "fp64" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1 and r["peak"] > 0
+    assert r["hbm"]["unit"] == "GB/s" and 0 < r["hbm"]["frac"] < 1
     e = d["e2e"]
     assert e["unit"] == d["unit"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert 0 < e["value"] <= d["value"] * 1.05
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["value"] > 0
-    for c in ("c1", "c2", "c3", "c5"):
-        assert d["latency"][c]["us_median"] > 0
+    assert d["clocks"]["samples"] > 0 and d["clocks"]["sm_mhz"] > 0
+    p = d["parity"]
+    assert p["systems"] >= 256 and p["iterations_equal"] == p["systems"]
+    assert p["lambda_rel_err_max"] <= 1e-10
+    rows = d["baseline_configs"]
+    assert rows["c1"]["symstair_1e-08"]["iterations_equal"]
+    for kind in ("jacobi", "stair", "symstair"):
+        for eps in ("1e-08", "0.0001"):
+            c2 = rows["c2"][f"{kind}_{eps}"]
+            assert c2["iterations_equal"] and c2["cpu"]["us_full_scope_1core"] > 0
+    assert len(rows["c5"]["kappa_sweep"]) == 12
+    assert all(r5["iterations_equal"] for r5 in rows["c5"]["kappa_sweep"])
+    assert d["c4_eps_1e-4"]["value"] > d["value"]
     # the reference's other bench rows and callers: direct baseline, SQP step, NMPC batch
     assert d["dense_baseline"]["all_ok"] and d["dense_baseline"]["max_rel_diff_vs_pcg"] < 1e-3
     assert d["latency"]["sqp_step_n2"]["kernel"] == "fused small"
     assert d["latency"]["nmpc_batch_n2"]["systems_per_s"] > 0
     assert d["roofline"]["onchip"]["l1tex_throughput_pct_of_peak"] > 0
+
+
+def test_reference_arm_multi_rank_launcher():
+    """`bench.py --impl reference --gpus 2` without torchrun in the environment
+    re-launches itself under torch.distributed.run with two ranks (the path the
+    driver's scaling run takes); rank 0 alone prints the one JSON line."""
+    d = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
+              "--batch", "16", "--ref-budget", "1"], timeout=300)
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
