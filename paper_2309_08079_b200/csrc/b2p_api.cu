@@ -476,11 +476,15 @@ void launch_form(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, T* S, T*
 constexpr int kErrOk = 0x7f7f7f7f;
 
 // Fused batched solve on device data: K1 formation -> K3 PCG (fused mode).
+// dz_dev (nullable): the one-CTA and small-block kernels also run the PPCG
+// finish (reconstruct_primal) in their epilogue; returns whether dz was
+// produced (else the caller launches the primal kernel).
 template <class T>
-void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, int kind,
+bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, int kind,
                        int order, const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
                        SysOut* outs_dev, int* errkey, double* trace_dev, int trace_cap,
-                       cudaStream_t st, bool time_it, const std::string& tag) {
+                       cudaStream_t st, bool time_it, const std::string& tag,
+                       void* dz_dev = nullptr) {
   const int K = k->N + 1, n = k->n;
   const size_t nn = static_cast<size_t>(n) * n, D = static_cast<size_t>(K) * n;
   const bool drift = cfg && cfg->check_residual_drift && cfg->variant == B2P_SEQUENTIAL;
@@ -586,7 +590,7 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       c->last_path = 3;
       c->phases = time_it;
       if (time_it) CK(cudaEventRecord(c->ev1, st));
-      return;
+      return false;
     }
   }
   const bool use_fc = fcG > 0 && env_int("B2P_FUSED", 1) &&
@@ -639,7 +643,7 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     c->last_path = 2;
     c->phases = time_it;
     if (time_it) CK(cudaEventRecord(c->ev1, st));
-    return;
+    return false;
   }
   if (!drift && env_int("B2P_FUSED", 1) && fused_supported<T>(K, n, k->m, kind)) {
     // persistent one-CTA-per-system K1+K3 kernel (fused_kernels.cu)
@@ -657,8 +661,9 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.e = static_cast<const T*>(kv.e);
     f.x_s = static_cast<const T*>(kv.x_s);
     f.x0 = static_cast<const T*>(kv.x0);
-    f.slot = static_cast<T*>(
-        ws_get(c, tag + "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n, k->m)));
+    f.dz_out = static_cast<T*>(dz_dev);
+    f.slot = static_cast<T*>(ws_get(
+        c, tag + "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n, k->m, dz_dev != nullptr)));
     f.timing = env_int("B2P_PHASE_TIMING", 0)
                    ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
                    : nullptr;
@@ -693,10 +698,11 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     c->last_path = 1;
     c->phases = time_it;
     if (time_it) CK(cudaEventRecord(c->ev1, st));
-    return;
+    return dz_dev != nullptr;
   }
   if (!drift && env_int("B2P_FUSED", 1) && env_int("B2P_SMALL", 1) &&
-      small_supported<T>(K, n, k->m, kind)) {
+      small_supported<T>(K, n, k->m, kind) &&
+      (!dz_dev || small_supported_dz<T>(K, n, k->m, kind))) {
     // small blocks (n, m <= 8): one CTA per system, all in shared memory
     // persistent CTAs, as many as fit co-resident (launch_small scales the SM count)
     const int grid = c->sm_count;
@@ -719,6 +725,7 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.out = outs_dev;
     f.trace = trace_dev;
     f.trace_cap = trace_cap;
+    f.dz_out = static_cast<T*>(dz_dev);
     f.epsilon = cfg ? cfg->epsilon : 1e-4;
     const int mi = cfg ? cfg->max_iter : 0;
     f.max_iter = mi > 0 ? mi : static_cast<int>(D);
@@ -747,7 +754,7 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     c->last_path = 4;
     c->phases = time_it;
     if (time_it) CK(cudaEventRecord(c->ev1, st));
-    return;
+    return dz_dev != nullptr;
   }
   c->last_path = 0;
   T* S = static_cast<T*>(ws_get(c, tag + "S", sizeof(T) * B * K * 3 * nn));
@@ -796,6 +803,7 @@ void solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   CK(launch_pcg<T>(p, st));
   c->launches++;
   if (time_it) CK(cudaEventRecord(c->ev1, st));
+  return false;
 }
 
 void check_cfg(const b2p_pcg_config* cfg) {
@@ -1430,13 +1438,17 @@ int solve_one(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
     double* dtr = nullptr;
     if (trace && cfg && cfg->collect_trace)
       dtr = static_cast<double*>(ws_get(c, "sv_tr", sizeof(double) * mi));
+    // the one-CTA / small-block kernels run reconstruct_primal in their
+    // epilogue (one launch for the whole SQP linear step); other paths launch
+    // the primal kernel after the solve
+    bool dz_done;
     if (dtype == B2P_F64)
-      solve_device_impl<double>(c, k, kv, 1, kind, order, cfg, dl0, dl, dout, ek, dtr, mi, st,
-                                true, "sv_");
+      dz_done = solve_device_impl<double>(c, k, kv, 1, kind, order, cfg, dl0, dl, dout, ek, dtr,
+                                          mi, st, true, "sv_", dz_out ? dob + oDz : nullptr);
     else
-      solve_device_impl<float>(c, k, kv, 1, kind, order, cfg, dl0, dl, dout, ek, dtr, mi, st,
-                               true, "sv_");
-    if (dz_out) {
+      dz_done = solve_device_impl<float>(c, k, kv, 1, kind, order, cfg, dl0, dl, dout, ek, dtr,
+                                         mi, st, true, "sv_", dz_out ? dob + oDz : nullptr);
+    if (dz_out && !dz_done) {
       // reconstruct_primal on the resident knots and multipliers. If the solve
       // failed, dz is never handed back.
       if (dtype == B2P_F64)

@@ -245,10 +245,12 @@ __host__ __device__ constexpr int fused_ls(int n) { return n * n + ((8 - (n * n)
 
 // per-CTA slot stride in elements, padded to 16 bytes (the TMA source must be aligned):
 // L [K][LS] | D [K][n n] | theta^-1 [K][n n] | gamma [K][n] | R^-1 [K][m m]
+// (| Q^-1 [K][n n] with the fused PPCG finish, keep_q)
 template <class T>
-__host__ __device__ inline size_t fused_slot_stride(int K, int n, int m) {
-  const size_t e = static_cast<size_t>(K) * fused_ls(n) + static_cast<size_t>(2) * K * n * n +
-                   static_cast<size_t>(K) * n + static_cast<size_t>(K) * m * m;
+__host__ __device__ inline size_t fused_slot_stride(int K, int n, int m, bool keep_q = false) {
+  const size_t e = static_cast<size_t>(K) * fused_ls(n) +
+                   static_cast<size_t>(keep_q ? 3 : 2) * K * n * n + static_cast<size_t>(K) * n +
+                   static_cast<size_t>(K) * m * m;
   const size_t a = 16 / sizeof(T);
   return (e + a - 1) / a * a;
 }
@@ -309,11 +311,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   auto colL = [&](int r) { return tbase + 64u + 32u * r; };
   // CTA-private slot (L2 resident): L and D (TMA-staged for the PCG phase),
   // theta^-1, gamma, R^-1
-  T* gL = p.slot + static_cast<size_t>(blockIdx.x) * fused_slot_stride<T>(K, NB, MB);
+  const bool keep_q = p.dz_out != nullptr;
+  T* gL = p.slot + static_cast<size_t>(blockIdx.x) * fused_slot_stride<T>(K, NB, MB, keep_q);
   T* gD = gL + static_cast<size_t>(K) * LS;
   T* gT = gD + static_cast<size_t>(K) * NN;
   T* gG = gT + static_cast<size_t>(K) * NN;  // gamma [K][NB]
   T* gR = gG + static_cast<size_t>(K) * NB;  // R_k^-1 [N][MB][MB]
+  T* gQ = gR + static_cast<size_t>(K) * MB * MB;  // Q_k^-1 [K][NB][NB] (fused finish only)
 
   for (int sys = blockIdx.x; sys < p.B; sys += gridDim.x) {
     const size_t nn = NN, nm = NB * MB, mm = MB * MB;
@@ -402,6 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           for (int i = 0; i < NB; ++i) {
             sQi[k * NN + i * NB + l] = x[i];
             qq += x[i] * sq[k * NB + i];
+            if (keep_q) gQ[static_cast<size_t>(k) * NN + i * NB + l] = x[i];
           }
           sqq[k * 16 + l] = qq;
         }
@@ -742,6 +747,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     }
     // r~ = Phi^-1 r, for every kind
     const bool corr_row = (p.kind == kSymStair) || (pbc & 1);
+    // the same-block products read su; quarter-warps past the horizon (pb >= K,
+    // results discarded) read sp instead: their clamped block is another
+    // warp's, whose su writes are only __syncwarp-ordered, while sp is
+    // barrier-ordered here
+    const T* sown = pb < K ? su : sp;
     auto precondition = [&]() {
       if (p.kind == kIdentity) {
 #pragma unroll
@@ -753,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       for (int c = 0; c < 2; ++c)
         if (pact) su[pbc * NB + pi + 7 * c] = rr[c];
       __syncwarp();
-      dots_reg2<T, NB>(ti, su + pbc * NB, tv);  // t = theta^-1 r
+      dots_reg2<T, NB>(ti, sown + pbc * NB, tv);  // t = theta^-1 r
       if (p.kind == kJacobi) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) rt[c] = tv[c];
@@ -777,7 +787,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       }
       __syncwarp();
       T uv[2];
-      dots_reg2<T, NB>(ti, su + pbc * NB, uv);  // theta^-1 u
+      dots_reg2<T, NB>(ti, sown + pbc * NB, uv);  // theta^-1 u
 #pragma unroll
       for (int c = 0; c < 2; ++c) rt[c] = corr_row ? uv[c] : tv[c];
     };
@@ -873,6 +883,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           p.lambda_out[static_cast<size_t>(sys) * K * NB + pbc * NB + pi + 7 * c] =
               converged ? lam[c] : best[c];
     }
+    if (keep_q && code == kOk) {
+      // The PPCG finish (reconstruct_primal, kkt.cpp:153-181)
+      // on the formation's Q_k^-1 / R_k^-1 (slot, L2) and this solve's lambda:
+      // half-warp h takes knots h, h + 32, lane i = row i,
+      //   dx_k = Q_k^-1 (-((q_k + lambda_k) - A_k' lambda_{k+1})),
+      //   du_k = R_k^-1 (-(r_k - B_k' lambda_{k+1})), dx_N = Q_N^-1 (-(q_N + lambda_N)).
+      __syncthreads();  // lambda (global) complete; sL is dead
+      const T* lamo = p.lambda_out + static_cast<size_t>(sys) * K * NB;
+      T* dz = p.dz_out + static_cast<size_t>(sys) * (static_cast<size_t>(K) * NB + static_cast<size_t>(N) * MB);
+      T* W = sL + h * 32;  // this half-warp's right-hand sides
+#pragma unroll 1
+      for (int r = 0; r < R; ++r) {
+        const int k = h + r * kHalfWarps;
+        const bool kv = k < K;
+        if (kv && lact) {
+          T at = T(0);
+          if (k < N) {
+#pragma unroll
+            for (int j = 0; j < NB; ++j) at += __ldg(As + static_cast<size_t>(k) * nn + j * NB + l) * lamo[(k + 1) * NB + j];
+          }
+          const T qk = __ldg(qs + k * NB + l) + lamo[k * NB + l];
+          W[l] = k < N ? -(qk - at) : -qk;
+        }
+        if (kv && k < N && l < MB) {
+          T bt = T(0);
+#pragma unroll
+          for (int j = 0; j < NB; ++j) bt += __ldg(Bs + static_cast<size_t>(k) * nm + j * MB + l) * lamo[(k + 1) * NB + j];
+          W[16 + l] = -(__ldg(rs + k * MB + l) - bt);
+        }
+        __syncwarp();
+        if (kv && lact) {
+          T sx = T(0);
+#pragma unroll
+          for (int j = 0; j < NB; ++j) sx += __ldcg(gQ + static_cast<size_t>(k) * NN + j * NB + l) * W[j];
+          dz[static_cast<size_t>(k) * (NB + MB) + l] = sx;
+        }
+        if (kv && k < N && l < MB) {
+          T su2 = T(0);
+#pragma unroll
+          for (int j = 0; j < MB; ++j) su2 += __ldcg(gR + static_cast<size_t>(k) * mm + j * MB + l) * W[16 + j];
+          dz[static_cast<size_t>(k) * (NB + MB) + NB + l] = su2;
+        }
+        __syncwarp();
+      }
+    }
     if (tid == 0) {
       SysOut o;
       o.code = code;
@@ -915,8 +970,13 @@ bool fused_supported(int K, int n, int m, int kind) {
 }
 
 template <class T>
-size_t fused_slot_elems(int K, int n, int m) {
-  return fused_slot_stride<T>(K, n, m);
+size_t fused_slot_elems(int K, int n, int m, bool keep_q) {
+  return fused_slot_stride<T>(K, n, m, keep_q);
+}
+
+template <class T>
+bool fused_supported_dz(int K, int n, int m, int kind) {
+  return fused_supported<T>(K, n, m, kind);
 }
 
 template <class T>
@@ -942,8 +1002,10 @@ cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st) {
 
 template bool fused_supported<double>(int, int, int, int);
 template bool fused_supported<float>(int, int, int, int);
-template size_t fused_slot_elems<double>(int, int, int);
-template size_t fused_slot_elems<float>(int, int, int);
+template size_t fused_slot_elems<double>(int, int, int, bool);
+template size_t fused_slot_elems<float>(int, int, int, bool);
+template bool fused_supported_dz<double>(int, int, int, int);
+template bool fused_supported_dz<float>(int, int, int, int);
 template cudaError_t launch_fused<double>(const FusedParams<double>&, int, cudaStream_t);
 template cudaError_t launch_fused<float>(const FusedParams<float>&, int, cudaStream_t);
 

@@ -82,14 +82,22 @@ struct FusedParams {
   T* gamma_out;
   T* theta_out;
   int form_only;
+  // the PPCG finish fused into the solve (one-CTA and small-block kernels):
+  // when non-null, every successfully solved system also gets
+  // dz = [x_0, u_0, ..., x_N] ([B][K n + N m]) from the formation's Q_k^-1 /
+  // R_k^-1 (reconstruct_primal, kkt.cpp:153-181)
+  T* dz_out;
 };
 template <class T> bool fused_supported(int K, int n, int m, int kind);
-template <class T> size_t fused_slot_elems(int K, int n, int m);
+// shared memory / slot need grows with dz_out (Q_k^-1 kept for the finish)
+template <class T> bool fused_supported_dz(int K, int n, int m, int kind);
+template <class T> size_t fused_slot_elems(int K, int n, int m, bool keep_q = false);
 template <class T> cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st);
 
 // Fused one-CTA kernel for small blocks (small_kernels.cu): n, m <= 8 padded
 // to powers of two, everything in shared memory (the SQP / NMPC shapes).
 template <class T> bool small_supported(int K, int n, int m, int kind);
+template <class T> bool small_supported_dz(int K, int n, int m, int kind);
 template <class T>
 cudaError_t launch_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st);
 

@@ -79,7 +79,7 @@ __device__ __forceinline__ T team_reduce(T v, T* red) {
 // shuffle-only reductions measured slower — rows per lane serialise). Vectors
 // live in U (the dead formation scratch).
 template <class T, int NP, int TEAM>
-__device__ void small_pcg(const FusedParams<T>& p, int sys, int n, int K, const T* sD,
+__device__ int small_pcg(const FusedParams<T>& p, int sys, int n, int K, const T* sD,
                           const T* sL, const T* sTi, const T* sG, T* U) {
   constexpr int NN = NP * NP;
   const int tid = threadIdx.x;
@@ -278,6 +278,70 @@ __device__ void small_pcg(const FusedParams<T>& p, int sys, int n, int K, const 
     o._pad = 0;
     p.out[sys] = o;
   }
+  return code;
+}
+
+// The PPCG finish (reconstruct_primal, kkt.cpp:153-181) on
+// the formation's resident Q_k^-1 / R_k^-1 and the solve's lambda: one lane
+// group per knot, lane i = row i,
+//   dx_k = Q_k^-1 (-((q_k + lambda_k) - A_k' lambda_{k+1})),
+//   du_k = R_k^-1 (-(r_k - B_k' lambda_{k+1})),   dx_N = Q_N^-1 (-(q_N + lambda_N)).
+// The right-hand sides are formed in the reference's association; the solve is
+// the explicit inverse the formation already holds (the reference factors with
+// LDLT: the same solution to rounding).
+template <class T, int NP, int MP, int TH>
+__device__ void small_finish(const FusedParams<T>& p, int sys, int n, int m, int K,
+                             const T* sQi, const T* sRi, T* W) {
+  constexpr int GW = group_width<NP, MP>(), kGroups = TH / GW;
+  constexpr int NN = NP * NP, MM = MP * MP;
+  const int N = K - 1, tid = threadIdx.x, g = tid / GW, l = tid % GW;
+  const T* lam = p.lambda_out + size_t(sys) * K * n;
+  const T* q = p.q + size_t(sys) * K * n;
+  const T* r = p.r + size_t(sys) * N * m;
+  const T* A = p.A + size_t(sys) * N * n * n;
+  const T* Bm = p.Bm + size_t(sys) * N * n * m;
+  T* dz = p.dz_out + size_t(sys) * (size_t(K) * n + size_t(N) * m);
+  T* wx = W + size_t(g) * (NP + MP);  // the group's right-hand sides
+  T* wu = wx + NP;
+  const int kTrips = (K + kGroups - 1) / kGroups;
+#pragma unroll 1
+  for (int t = 0; t < kTrips; ++t) {
+    const int k = g + t * kGroups;
+    const bool kv = k < K;
+    if (kv && l < NP) {  // pad rows: exact zeros
+      T rx = T(0);
+      if (l < n) {
+        T at = T(0);
+        if (k < N)  // (A_k' lambda_{k+1})_l
+          for (int j = 0; j < n; ++j) at += A[size_t(k) * n * n + j * n + l] * lam[(k + 1) * n + j];
+        rx = k < N ? -((q[k * n + l] + lam[k * n + l]) - at) : -(q[k * n + l] + lam[k * n + l]);
+      }
+      wx[l] = rx;
+    }
+    if (kv && l < MP) {
+      T ru = T(0);
+      if (k < N && l < m) {
+        T bt = T(0);
+        for (int j = 0; j < n; ++j) bt += Bm[size_t(k) * n * m + j * m + l] * lam[(k + 1) * n + j];
+        ru = -(r[k * m + l] - bt);
+      }
+      wu[l] = ru;
+    }
+    __syncwarp();
+    if (kv && l < n) {
+      T s = T(0);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) s += sQi[size_t(k) * NN + l * NP + j] * wx[j];
+      dz[size_t(k) * (n + m) + l] = s;
+    }
+    if (kv && k < N && l < m) {
+      T s = T(0);
+#pragma unroll
+      for (int j = 0; j < MP; ++j) s += sRi[size_t(k) * MM + l * MP + j] * wu[j];
+      dz[size_t(k) * (n + m) + n + l] = s;
+    }
+    __syncwarp();
+  }
 }
 
 // BATCH = true: the throughput build for batches (registers capped so 4 / 3 CTAs
@@ -301,13 +365,17 @@ __global__ void __launch_bounds__(kSmallThreads, (!BATCH ? 1 : (NP <= 2 ? 4 : (N
   T* sL = sD + size_t(K) * NN;
   T* sTi = sL + size_t(K) * NN;
   T* sG = sTi + size_t(K) * NN;
-  T* U = sG + size_t(K) * NP;
+  // with the fused finish (dz_out) Q_k^-1 and R_k^-1 stay resident past the PCG
+  const bool keep = p.dz_out != nullptr;
+  const size_t NR = size_t(N > 0 ? N : 1);
+  T* sKeep = sG + size_t(K) * NP;
+  T* U = sKeep + (keep ? size_t(K) * NN + NR * MM : 0);
   // formation scratch
-  T* sQi = U;                                  // [K][NP][NP]
-  T* sqq = sQi + size_t(K) * NN;               // [K][NP]
-  T* sRi = sqq + size_t(K) * NP;               // [N][MP][MP]
-  T* srr = sRi + size_t(N > 0 ? N : 1) * MM;   // [N][MP]
-  T* tiles = srr + size_t(N > 0 ? N : 1) * MP;
+  T* sQi = keep ? sKeep : U;                             // [K][NP][NP]
+  T* sRi = keep ? sKeep + size_t(K) * NN : U + size_t(K) * (NN + NP);  // [N][MP][MP]
+  T* sqq = keep ? U : sQi + size_t(K) * NN;              // [K][NP]
+  T* srr = keep ? sqq + size_t(K) * NP : sRi + NR * MM;  // [N][MP]
+  T* tiles = srr + NR * MP;
   T* tLr = tiles + size_t(g) * L::tile;
   T* tLi = tLr + NN;
   T* tSym = tLi + NN;
@@ -542,7 +610,11 @@ __global__ void __launch_bounds__(kSmallThreads, (!BATCH ? 1 : (NP <= 2 ? 4 : (N
 
     // ================================================================ P
     if (tm) tm[3] = small_gtimer();
-    small_pcg<T, NP, kSmallThreads>(p, sys, n, K, sD, sL, sTi, sG, U);
+    const int code = small_pcg<T, NP, kSmallThreads>(p, sys, n, K, sD, sL, sTi, sG, U);
+    if (keep && code == kOk) {
+      __syncthreads();  // lambda (global) and the PCG vectors (U) complete
+      small_finish<T, NP, MP, kSmallThreads>(p, sys, n, m, K, sQi, sRi, U);
+    }
     if (tm) tm[4] = small_gtimer();
   }
 }
@@ -553,16 +625,18 @@ int pad_pow2(int v) { return v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : v <= 8 ? 8 :
 // [K][NP], then the formation scratch (Q^-1, Q^-1 q, R^-1, R^-1 r, the
 // per-group inverse tiles and, when `staged`, the system's knot data) aliased
 // by the PCG vectors.
-size_t small_bytes_rt(int NP, int MP, int K, bool staged, int threads) {
+size_t small_bytes_rt(int NP, int MP, int K, bool staged, int threads, bool keep = false) {
   const size_t NN = size_t(NP) * NP, MM = size_t(MP) * MP, N = K > 1 ? K - 1 : 0;
+  const size_t kept = keep ? size_t(K) * NN + std::max<size_t>(N, 1) * MM : 0;
   const int GW = std::max(2, std::max(NP, MP));
   const size_t tile = 3 * NN + NP + 2 * MM + MP;
   const size_t stg =
       staged ? size_t(K) * (NN + NP) + N * (MM + MP + NN + NP * MP + NP) + 2 * NP : 0;
   const size_t form_t = size_t(K) * (NN + NP) + std::max<size_t>(N, 1) * (MM + MP) +
-                        size_t(threads / GW) * tile + stg;
-  const size_t pcg = size_t(8) * K * NP + 64;
-  return sizeof(double) * (size_t(K) * (3 * NN + NP) + std::max(form_t, pcg));
+                        size_t(threads / GW) * tile + stg - (keep ? kept : 0);
+  const size_t fin = keep ? size_t(threads / GW) * (NP + MP) : 0;
+  const size_t pcg = std::max(size_t(8) * K * NP + 64, fin);
+  return sizeof(double) * (size_t(K) * (3 * NN + NP) + kept + std::max(form_t, pcg));
 }
 
 int small_threads(int NP, int K) { return K * NP <= 128 ? kSmallThreadsLo : kSmallThreadsHi; }
@@ -571,8 +645,9 @@ constexpr size_t kSmallSmemCap = 227 * 1024 - 1024;
 
 template <class T, int NP, int MP, int TH>
 cudaError_t go_small_th(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
-  const bool staged = small_bytes_rt(NP, MP, p.K, true, TH) <= kSmallSmemCap;
-  const size_t smem = small_bytes_rt(NP, MP, p.K, staged, TH);
+  const bool keep = p.dz_out != nullptr;
+  const bool staged = small_bytes_rt(NP, MP, p.K, true, TH, keep) <= kSmallSmemCap;
+  const size_t smem = small_bytes_rt(NP, MP, p.K, staged, TH, keep);
   auto kern = p.B > 1 ? k_fused_small<T, NP, MP, true, TH> : k_fused_small<T, NP, MP, false, TH>;
   cudaError_t e = ensure_max_smem(kern, smem);
   if (e != cudaSuccess) return e;
@@ -614,6 +689,13 @@ bool small_supported(int K, int n, int m, int kind) {
 }
 
 template <class T>
+bool small_supported_dz(int K, int n, int m, int kind) {
+  if (!small_supported<T>(K, n, m, kind)) return false;
+  const int NP = pad_pow2(n), MP = pad_pow2(m);
+  return small_bytes_rt(NP, MP, K, false, small_threads(NP, K), true) <= kSmallSmemCap;
+}
+
+template <class T>
 cudaError_t launch_small(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
   if constexpr (sizeof(T) == 8) {
     switch (pad_pow2(n)) {
@@ -628,6 +710,8 @@ cudaError_t launch_small(const FusedParams<T>& p, int n, int m, int grid, cudaSt
 
 template bool small_supported<double>(int, int, int, int);
 template bool small_supported<float>(int, int, int, int);
+template bool small_supported_dz<double>(int, int, int, int);
+template bool small_supported_dz<float>(int, int, int, int);
 template cudaError_t launch_small<double>(const FusedParams<double>&, int, int, int, cudaStream_t);
 template cudaError_t launch_small<float>(const FusedParams<float>&, int, int, int, cudaStream_t);
 
