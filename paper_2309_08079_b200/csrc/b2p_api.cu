@@ -464,7 +464,7 @@ void launch_form(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, T* S, T*
     g.form_only = 1;
     g.max_iter = 1;
     CK(cudaMemsetAsync(S, 0, sizeof(T) * static_cast<size_t>(B) * K * 3 * k->n * k->n, st));
-    CK(launch_fused<T>(g, grid, st));
+    CK(launch_fused<T>(g, k->n, k->m, grid, st));
     c->launches++;
     return;
   }
@@ -693,7 +693,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       CK(cudaEventRecord(c->ev0, st));
       CK(cudaEventRecord(c->ev2, st));  // no separate formation launch
     }
-    CK(launch_fused<T>(f, grid, st));
+    CK(launch_fused<T>(f, n, k->m, grid, st));
     c->launches++;
     c->last_path = 1;
     c->phases = time_it;

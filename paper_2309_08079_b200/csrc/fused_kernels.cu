@@ -26,6 +26,7 @@
 //      16 warp partials: bit-reproducible, no atomics.
 #include "kernels.h"
 #include "hw_dense.cuh"
+#include "tmem.cuh"
 
 namespace b2p {
 namespace {
@@ -41,7 +42,8 @@ struct FLayout {
   static constexpr int LD = Odd<NB>::v;
   static constexpr int LDM = Odd<MB>::v;
   // tW: transposes / AQ / Lr tile; tX: L^-T tile, aliased by B R^-1; rd[16], v[16]
-  static constexpr int per_hw = NB * LD + NB * NB + 32;
+  static constexpr int TX = NB * NB > 128 ? NB * NB : 128;  // >= two 8x8 R^-1 tiles
+  static constexpr int per_hw = NB * LD + TX + 32;
   __host__ __device__ static int oQi(int) { return 0; }
   __host__ __device__ static int oqq(int K) { return K * NB * NB; }
   __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
@@ -97,146 +99,11 @@ __device__ __forceinline__ void mbar_wait(unsigned mbar_addr, unsigned& phase) {
 
 // ---- Tensor memory (TMEM) as a third on-chip operand store for the PCG
 // phase: 512 columns x 128 lanes x 32 bit; thread t of warp w owns TMEM lane
-// 32*(w%4) + t%32 and columns [128*(w/4), 128*(w/4) + 128): D_b row l and L_b
-// row l of its R = 2 block rows, 32 columns (14 doubles + pad) each.
+// 32*(w%4) + t%32 and columns [128*(w/4), 128*(w/4) + 128): rows pi and
+// pi + NB/2 of D_b and of L_b, 32 columns (NB <= 16 doubles) each (tmem.cuh).
 // Measured tcgen05.ld throughput ~390 B/clk/SM vs 128 B/clk for shared memory
 // (scripts/micro/tmem_bench.cu), so the row products come from TMEM and only
 // the column products R_b = L_{b+1}' read shared memory.
-__device__ __forceinline__ void tm_st_row14(unsigned taddr, const double (&v)[14]) {
-  unsigned u[28];
-#pragma unroll
-  for (int j = 0; j < 14; ++j) {
-    u[2 * j] = static_cast<unsigned>(__double2loint(v[j]));
-    u[2 * j + 1] = static_cast<unsigned>(__double2hiint(v[j]));
-  }
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15,%16};\n" ::"r"(taddr),
-      "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]),
-      "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]), "r"(u[15])
-      : "memory");
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr + 16),
-      "r"(u[16]), "r"(u[17]), "r"(u[18]), "r"(u[19]), "r"(u[20]), "r"(u[21]), "r"(u[22]), "r"(u[23])
-      : "memory");
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(taddr + 24),
-               "r"(u[24]), "r"(u[25]), "r"(u[26]), "r"(u[27])
-               : "memory");
-}
-__device__ __forceinline__ void tm_ld_row14(unsigned taddr, double (&v)[14]) {
-  // No "memory" clobbers: the loads only write registers, so the compiler may
-  // keep scheduling shared-memory loads around them; the wait takes every
-  // destination register as an in/out operand, which keeps all consumers
-  // after it.
-  unsigned u[28];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-      "%15}, [%16];\n"
-      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
-        "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
-        "=r"(u[14]), "=r"(u[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-               : "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]),
-                 "=r"(u[22]), "=r"(u[23])
-               : "r"(taddr + 16));
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
-               : "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27])
-               : "r"(taddr + 24));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]),
-                 "+r"(u[7]), "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]),
-                 "+r"(u[13]), "+r"(u[14]), "+r"(u[15]), "+r"(u[16]), "+r"(u[17]), "+r"(u[18]),
-                 "+r"(u[19]), "+r"(u[20]), "+r"(u[21]), "+r"(u[22]), "+r"(u[23]), "+r"(u[24]),
-                 "+r"(u[25]), "+r"(u[26]), "+r"(u[27]));
-#pragma unroll
-  for (int j = 0; j < 14; ++j) v[j] = __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j]));
-}
-// (o0, o1) = (row t0 . x, row t1 . x) for two 14-double TMEM rows of the calling
-// thread's lane against one 16-byte aligned shared vector: each broadcast x pair
-// serves both rows. Loaded in two column halves (8 + 6 doubles) to bound the
-// live registers; per row the same two-accumulator order as dot_rm.
-__device__ __forceinline__ void tm_dot2_row14(unsigned t0, unsigned t1, const double* x,
-                                              double& o0, double& o1) {
-  double a0 = 0.0, c0 = 0.0, a1 = 0.0, c1 = 0.0;
-  {
-    unsigned u[16], w[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-        "%15}, [%16];\n"
-        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
-          "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
-          "=r"(u[14]), "=r"(u[15])
-        : "r"(t0));
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-        "%15}, [%16];\n"
-        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
-          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
-          "=r"(w[14]), "=r"(w[15])
-        : "r"(t1));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-                 : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]),
-                   "+r"(u[6]), "+r"(u[7]), "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]),
-                   "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15]), "+r"(w[0]), "+r"(w[1]),
-                   "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7]),
-                   "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]),
-                   "+r"(w[14]), "+r"(w[15]));
-#pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(x + j);
-      a0 += __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j])) * v.x;
-      c0 += __hiloint2double(static_cast<int>(u[2 * j + 3]), static_cast<int>(u[2 * j + 2])) * v.y;
-      a1 += __hiloint2double(static_cast<int>(w[2 * j + 1]), static_cast<int>(w[2 * j])) * v.x;
-      c1 += __hiloint2double(static_cast<int>(w[2 * j + 3]), static_cast<int>(w[2 * j + 2])) * v.y;
-    }
-  }
-  {
-    unsigned u[12], w[12];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                 : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]),
-                   "=r"(u[6]), "=r"(u[7])
-                 : "r"(t0 + 16));
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11])
-                 : "r"(t0 + 24));
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
-                   "=r"(w[6]), "=r"(w[7])
-                 : "r"(t1 + 16));
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11])
-                 : "r"(t1 + 24));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-                 : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]),
-                   "+r"(u[6]), "+r"(u[7]), "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]),
-                   "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]),
-                   "+r"(w[6]), "+r"(w[7]), "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]));
-#pragma unroll
-    for (int j = 0; j < 6; j += 2) {
-      const double2 v = *reinterpret_cast<const double2*>(x + 8 + j);
-      a0 += __hiloint2double(static_cast<int>(u[2 * j + 1]), static_cast<int>(u[2 * j])) * v.x;
-      c0 += __hiloint2double(static_cast<int>(u[2 * j + 3]), static_cast<int>(u[2 * j + 2])) * v.y;
-      a1 += __hiloint2double(static_cast<int>(w[2 * j + 1]), static_cast<int>(w[2 * j])) * v.x;
-      c1 += __hiloint2double(static_cast<int>(w[2 * j + 3]), static_cast<int>(w[2 * j + 2])) * v.y;
-    }
-  }
-  o0 = a0 + c0;
-  o1 = a1 + c1;
-}
-
-// sum_j m[j] x[j] (m in registers, x a 16-byte aligned shared vector), two partial sums
-template <int NB>
-__device__ __forceinline__ double dot_rm(const double (&m)[NB], const double* x) {
-  double a = 0.0, c = 0.0;
-#pragma unroll
-  for (int j = 0; j < NB; j += 2) {
-    const double2 v = *reinterpret_cast<const double2*>(x + j);
-    a += m[j] * v.x;
-    c += m[j + 1] * v.y;
-  }
-  return a + c;
-}
 
 // Block stride (elements) of L in the slot and in shared memory: n*n padded to
 // 8 mod 32 doubles, so the four quarter-warps of a PCG warp (consecutive block
@@ -255,9 +122,15 @@ __host__ __device__ inline size_t fused_slot_stride(int K, int n, int m, bool ke
   return (e + a - 1) / a * a;
 }
 
-template <class T, int NB, int MB, int R>
+// NB: the state dimension n (even, <= 16); MB: the control dimension padded
+// (R^-1 tiles and the slot use MB; EXM: m == MB exactly, else the runtime
+// p.m_rt <= MB with identity-padded R and zero-padded B, r — the pad terms add
+// exact zeros after the real ones, so every sum equals the unpadded one).
+template <class T, int NB, int MB, int R, bool EXM>
 __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
-  static_assert(NB == 14 && sizeof(T) == 8, "TMEM row layout is written for n = 14, fp64");
+  static_assert(sizeof(T) == 8 && NB % 2 == 0 && NB <= 16 && MB <= 8,
+                "one-CTA kernel: fp64, even n <= 16, m <= 8");
+  constexpr int H = NB / 2;  // PCG rows per thread: pi and pi + H
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using FL = FLayout<T, NB, MB>;
   constexpr int NN = NB * NB;
@@ -320,11 +193,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   T* gQ = gR + static_cast<size_t>(K) * MB * MB;  // Q_k^-1 [K][NB][NB] (fused finish only)
 
   for (int sys = blockIdx.x; sys < p.B; sys += gridDim.x) {
-    const size_t nn = NN, nm = NB * MB, mm = MB * MB;
+    const int m = EXM ? MB : p.m_rt;  // control dimension of the input arrays
+    const size_t nn = NN, nm = static_cast<size_t>(NB) * m, mm = MB * MB;  // mm: padded R^-1
     const T* Qs = p.Q + static_cast<size_t>(sys) * K * nn;
     const T* qs = p.q + static_cast<size_t>(sys) * K * NB;
-    const T* Rs = p.R + static_cast<size_t>(sys) * N * mm;
-    const T* rs = p.r + static_cast<size_t>(sys) * N * MB;
+    const T* Rs = p.R + static_cast<size_t>(sys) * N * m * m;
+    const T* rs = p.r + static_cast<size_t>(sys) * N * m;
     const T* As = p.A + static_cast<size_t>(sys) * N * nn;
     const T* Bs = p.Bm + static_cast<size_t>(sys) * N * nm;
     const T* es = p.e + static_cast<size_t>(sys) * N * NB;
@@ -340,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     T* tW = hw;
     T* tX = tW + NB * LD;
     T* tBR = tX;  // B R^-1 (stride LDM) is dead before the theta inverse needs tX
-    T* rd = tX + NB * NB;
+    T* rd = tX + FL::TX;
     const int lr = lact ? l : NB - 1;
     int fkey = 0x7fffffff;
 
@@ -422,9 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       const int kc = kv ? k : N - 1;
       const int lm = ls < MB ? ls : MB - 1;
       T ra[MB], x[MB];
-      const T* Rr = Rs + static_cast<size_t>(kc) * mm + lm * MB;
+      const T* Rr = Rs + static_cast<size_t>(kc) * m * m + lm * m;
 #pragma unroll
-      for (int i = 0; i < MB; ++i) ra[i] = __ldg(Rr + i);
+      for (int i = 0; i < MB; ++i)  // identity pad rows / columns past m
+        ra[i] = (EXM || (lm < m && i < m)) ? __ldg(Rr + i) : (lm == i ? T(1) : T(0));
       const int f = g8_spd_inverse<T, MB>(ra, tW + sub * 64, tX + sub * 64, rd + sub * 8, ls, x);
       if (kv && f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
       if (kv && ls < MB) {
@@ -432,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int i = 0; i < MB; ++i) {
           gR[static_cast<size_t>(k) * mm + i * MB + ls] = x[i];
-          rr += x[i] * rs[k * MB + i];
+          rr += x[i] * ((EXM || i < m) ? rs[k * m + i] : T(0));
         }
         srr[k * 8 + ls] = rr;
       }
@@ -476,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       // R_k^-1 (from the slot, 8-byte aligned) -> the tW tile the same way
       T brow[MB];
 #pragma unroll
-      for (int q = 0; q < MB; ++q) brow[q] = __ldg(Bk + lr * MB + q);
+      for (int q = 0; q < MB; ++q) brow[q] = (EXM || q < m) ? __ldg(Bk + lr * m + q) : T(0);
       {
         const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(tX));
         for (int c = l; c < NN / 2; c += 16)
@@ -602,7 +477,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // proxy (TMA) below: order them before the barrier
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     if (tm) tm[2] = gtimer();
-    if (l == 0 && fkey != 0x7fffffff) atomicMin(&s_err, fkey);
+    // the R^-1 pass runs two 8-lane groups per half-warp (knots h, h + 32): each
+    // group's first lane reports its own (group-uniform) failures
+    if ((l & 7) == 0 && fkey != 0x7fffffff) atomicMin(&s_err, fkey);
     __syncthreads();
     if (s_err != 0x7fffffff) {
       if (tid == 0) {
@@ -627,11 +504,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     const int pq = lane >> 3;  // quarter-warp
     const int pi = lane & 7;   // row pair (pi, pi + 7); lane 7 of each quarter idles
     const int pb = 4 * (tid >> 5) + pq;
-    const bool pact = pi < 7 && pb < K;
+    const bool pact = pi < H && pb < K;
     const int pbc = pb < K ? pb : K - 1;            // clamped block row
     const int pbl = pbc > 0 ? pbc - 1 : 0;          // neighbours, clamped into [0, K):
     const int pbn = pbc + 1 < K ? pbc + 1 : K - 1;  // edge products are discarded
-    const int pr = pi < 7 ? pi : 6;                 // clamped row (idle lanes)
+    const int pr = pi < H ? pi : H - 1;             // clamped row (idle lanes)
     {
       // stage D and L from the slot (one TMA bulk copy each), then every thread
       // moves its own rows into its TMEM lane
@@ -650,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     T lam[2], rr[2], rt[2], pp[2], spv[2], best[2], gam[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const int row = pr + 7 * c;
+      const int row = pr + H * c;
       // theta^-1 row, stored transposed by F2 (bitwise symmetric)
 #pragma unroll
       for (int j = 0; j < NB; ++j) ti[c][j] = __ldcg(gT + static_cast<size_t>(pbc) * NN + j * NB + row);
@@ -660,31 +537,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     }
     mbar_wait(mbar_addr, mbar_phase);
     {
-      T m[NB];
+      T mrow[NB];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const T* Dr = sD + static_cast<size_t>(pbc) * NN + (pr + 7 * c) * NB;
+        const T* Dr = sD + static_cast<size_t>(pbc) * NN + (pr + H * c) * NB;
 #pragma unroll
         for (int j = 0; j < NB; j += 2) {
           const double2 v = *reinterpret_cast<const double2*>(Dr + j);
-          m[j] = v.x;
-          m[j + 1] = v.y;
+          mrow[j] = v.x;
+          mrow[j + 1] = v.y;
         }
-        tm_st_row14(colD(c), m);
-        const T* Lr = sL + static_cast<size_t>(pbc) * LS + (pr + 7 * c) * NB;
+        tm::st_row<NB>(colD(c), mrow);
+        const T* Lr = sL + static_cast<size_t>(pbc) * LS + (pr + H * c) * NB;
 #pragma unroll
         for (int j = 0; j < NB; j += 2) {
           const double2 v = *reinterpret_cast<const double2*>(Lr + j);
-          m[j] = v.x;
-          m[j + 1] = v.y;
+          mrow[j] = v.x;
+          mrow[j + 1] = v.y;
         }
-        tm_st_row14(colL(c), m);
+        tm::st_row<NB>(colL(c), mrow);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     }
 #pragma unroll
     for (int c = 0; c < 2; ++c)
-      if (pact) sp[pbc * NB + pi + 7 * c] = lam[c];
+      if (pact) sp[pbc * NB + pi + H * c] = lam[c];
     __syncthreads();  // sD consumed: the next system's Q may land in [0, K*NN)
     if (tm) tm[3] = gtimer();
     {
@@ -706,8 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         // per-field contiguous ranges of the next system (16-byte aligned inside)
         const T* base[9] = {p.Q, p.q, p.R, p.r, p.A, p.Bm, p.e, p.x_s, p.x0};
         const size_t per[9] = {static_cast<size_t>(K) * NN, static_cast<size_t>(K) * NB,
-                               static_cast<size_t>(N) * MB * MB, static_cast<size_t>(N) * MB,
-                               static_cast<size_t>(N) * NN, static_cast<size_t>(N) * NB * MB,
+                               static_cast<size_t>(N) * m * m, static_cast<size_t>(N) * m,
+                               static_cast<size_t>(N) * NN, static_cast<size_t>(N) * NB * m,
                                static_cast<size_t>(N) * NB, NB, NB};
         const char* lo = reinterpret_cast<const char*>(base[tid] + nsys * per[tid]);
         const char* hi = lo + per[tid] * sizeof(T);
@@ -725,8 +602,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // on in-bounds shared memory and discarded by the selects.
     auto Srows = [&](const T* x, T (&y)[2]) {
       T sd[2], sl[2], sr[2];
-      tm_dot2_row14(colD(0), colD(1), x + pbc * NB, sd[0], sd[1]);  // D_b rows (TMEM)
-      tm_dot2_row14(colL(0), colL(1), x + pbl * NB, sl[0], sl[1]);  // L_b rows (TMEM)
+      tm::dot2_row<NB>(colD(0), colD(1), x + pbc * NB, sd[0], sd[1]);  // D_b rows (TMEM)
+      tm::dot2_row<NB>(colL(0), colL(1), x + pbl * NB, sl[0], sl[1]);  // L_b rows (TMEM)
       dots_col2<T, NB, LS>(sL + static_cast<size_t>(pbn) * LS + pr, x + pbn * NB, sr);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -761,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       T tv[2];
 #pragma unroll
       for (int c = 0; c < 2; ++c)
-        if (pact) su[pbc * NB + pi + 7 * c] = rr[c];
+        if (pact) su[pbc * NB + pi + H * c] = rr[c];
       __syncwarp();
       dots_reg2<T, NB>(ti, sown + pbc * NB, tv);  // t = theta^-1 r
       if (p.kind == kJacobi) {
@@ -771,11 +648,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       }
 #pragma unroll
       for (int c = 0; c < 2; ++c)
-        if (pact) st[pbc * NB + pi + 7 * c] = tv[c];
+        if (pact) st[pbc * NB + pi + H * c] = tv[c];
       __syncthreads();
       // u = r - L_b t_{b-1} - R_b t_{b+1}
       T sl[2], sr[2];
-      tm_dot2_row14(colL(0), colL(1), st + pbl * NB, sl[0], sl[1]);
+      tm::dot2_row<NB>(colL(0), colL(1), st + pbl * NB, sl[0], sl[1]);
       dots_col2<T, NB, LS>(sL + static_cast<size_t>(pbn) * LS + pr, st + pbn * NB, sr);
       __syncwarp();  // every lane has read its block's r from su
 #pragma unroll
@@ -783,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         T v = rr[c];
         if (pbc > 0) v -= sl[c];
         if (pbc + 1 < K) v -= sr[c];
-        if (pact) su[pbc * NB + pi + 7 * c] = v;
+        if (pact) su[pbc * NB + pi + H * c] = v;
       }
       __syncwarp();
       T uv[2];
@@ -813,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     } else {
 #pragma unroll
       for (int c = 0; c < 2; ++c)
-        if (pact) sp[pbc * NB + pi + 7 * c] = pp[c];
+        if (pact) sp[pbc * NB + pi + H * c] = pp[c];
       __syncthreads();
       for (int it = 1; it <= p.max_iter; ++it) {
         T up = T(0);
@@ -870,7 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           pp[c] = rt[c] + beta * pp[c];
-          if (pact) sp[pbc * NB + pi + 7 * c] = pp[c];
+          if (pact) sp[pbc * NB + pi + H * c] = pp[c];
         }
         eta = eta_p;
         __syncthreads();
@@ -880,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
       for (int c = 0; c < 2; ++c)
         if (pact)
-          p.lambda_out[static_cast<size_t>(sys) * K * NB + pbc * NB + pi + 7 * c] =
+          p.lambda_out[static_cast<size_t>(sys) * K * NB + pbc * NB + pi + H * c] =
               converged ? lam[c] : best[c];
     }
     if (keep_q && code == kOk) {
@@ -891,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       //   du_k = R_k^-1 (-(r_k - B_k' lambda_{k+1})), dx_N = Q_N^-1 (-(q_N + lambda_N)).
       __syncthreads();  // lambda (global) complete; sL is dead
       const T* lamo = p.lambda_out + static_cast<size_t>(sys) * K * NB;
-      T* dz = p.dz_out + static_cast<size_t>(sys) * (static_cast<size_t>(K) * NB + static_cast<size_t>(N) * MB);
+      T* dz = p.dz_out + static_cast<size_t>(sys) * (static_cast<size_t>(K) * NB + static_cast<size_t>(N) * m);
       T* W = sL + h * 32;  // this half-warp's right-hand sides
 #pragma unroll 1
       for (int r = 0; r < R; ++r) {
@@ -906,24 +783,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           const T qk = __ldg(qs + k * NB + l) + lamo[k * NB + l];
           W[l] = k < N ? -(qk - at) : -qk;
         }
-        if (kv && k < N && l < MB) {
+        if (kv && k < N && l < MB) {  // pad entries: exact zeros
           T bt = T(0);
+          if (EXM || l < m) {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) bt += __ldg(Bs + static_cast<size_t>(k) * nm + j * MB + l) * lamo[(k + 1) * NB + j];
-          W[16 + l] = -(__ldg(rs + k * MB + l) - bt);
+            for (int j = 0; j < NB; ++j) bt += __ldg(Bs + static_cast<size_t>(k) * nm + j * m + l) * lamo[(k + 1) * NB + j];
+          }
+          W[16 + l] = (EXM || l < m) ? -(__ldg(rs + k * m + l) - bt) : T(0);
         }
         __syncwarp();
         if (kv && lact) {
           T sx = T(0);
 #pragma unroll
           for (int j = 0; j < NB; ++j) sx += __ldcg(gQ + static_cast<size_t>(k) * NN + j * NB + l) * W[j];
-          dz[static_cast<size_t>(k) * (NB + MB) + l] = sx;
+          dz[static_cast<size_t>(k) * (NB + m) + l] = sx;
         }
-        if (kv && k < N && l < MB) {
+        if (kv && k < N && l < m) {
           T su2 = T(0);
 #pragma unroll
           for (int j = 0; j < MB; ++j) su2 += __ldcg(gR + static_cast<size_t>(k) * mm + j * MB + l) * W[16 + j];
-          dz[static_cast<size_t>(k) * (NB + MB) + NB + l] = su2;
+          dz[static_cast<size_t>(k) * (NB + m) + NB + l] = su2;
         }
         __syncwarp();
       }
@@ -960,18 +839,45 @@ size_t fused_smem_bytes(int K) {
   return std::max(pcg, form);
 }
 
+// (n, m) -> the compiled shape: (14, 7) exactly (the BASELINE iiwa shape),
+// else even n in [10, 16] with m <= 8 padded to MB = 4 or 8 (runtime m).
+template <class F>
+bool with_fused_shape(int n, int m, F&& f) {
+  using std::integral_constant;
+  if (n == 14 && m == 7) return f(integral_constant<int, 14>{}, integral_constant<int, 7>{}, std::true_type{});
+  if (m < 1 || m > 8) return false;
+  const bool m4 = m <= 4;
+  switch (n) {
+    case 10: return m4 ? f(integral_constant<int, 10>{}, integral_constant<int, 4>{}, std::false_type{})
+                       : f(integral_constant<int, 10>{}, integral_constant<int, 8>{}, std::false_type{});
+    case 12: return m4 ? f(integral_constant<int, 12>{}, integral_constant<int, 4>{}, std::false_type{})
+                       : f(integral_constant<int, 12>{}, integral_constant<int, 8>{}, std::false_type{});
+    case 14: return m4 ? f(integral_constant<int, 14>{}, integral_constant<int, 4>{}, std::false_type{})
+                       : f(integral_constant<int, 14>{}, integral_constant<int, 8>{}, std::false_type{});
+    case 16: return m4 ? f(integral_constant<int, 16>{}, integral_constant<int, 4>{}, std::false_type{})
+                       : f(integral_constant<int, 16>{}, integral_constant<int, 8>{}, std::false_type{});
+  }
+  return false;
+}
+
 template <class T>
 bool fused_supported(int K, int n, int m, int kind) {
-  if (!(n == 14 && m == 7)) return false;
   if (sizeof(T) != 8) return false;
   if (kind == kPoly) return false;
   if (K < 2 || K > 2 * kHalfWarps) return false;
-  return fused_smem_bytes<T, 14, 7>(K) + 64 <= 227 * 1024;
+  return with_fused_shape(n, m, [&](auto nb, auto mb, auto) {
+    return fused_smem_bytes<T, decltype(nb)::value, decltype(mb)::value>(K) + 64 <= 227 * 1024;
+  });
 }
 
 template <class T>
 size_t fused_slot_elems(int K, int n, int m, bool keep_q) {
-  return fused_slot_stride<T>(K, n, m, keep_q);
+  int MB = m;
+  with_fused_shape(n, m, [&](auto, auto mb, auto) {
+    MB = decltype(mb)::value;
+    return true;
+  });
+  return fused_slot_stride<T>(K, n, MB, keep_q);
 }
 
 template <class T>
@@ -980,21 +886,24 @@ bool fused_supported_dz(int K, int n, int m, int kind) {
 }
 
 template <class T>
-cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st) {
+cudaError_t launch_fused(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st) {
   if constexpr (sizeof(T) == 8) {
-    const size_t smem = fused_smem_bytes<T, 14, 7>(p.K);
-    if (p.K <= kHalfWarps) {
-      auto kern = k_fused_cta<T, 14, 7, 1>;
-      cudaError_t e = ensure_max_smem(kern, smem);
-      if (e != cudaSuccess) return e;
-      kern<<<grid, kThreads, smem, st>>>(p);
-    } else {
-      auto kern = k_fused_cta<T, 14, 7, 2>;
-      cudaError_t e = ensure_max_smem(kern, smem);
-      if (e != cudaSuccess) return e;
-      kern<<<grid, kThreads, smem, st>>>(p);
-    }
-    return cudaGetLastError();
+    cudaError_t err = cudaErrorNotSupported;
+    FusedParams<T> q = p;
+    q.m_rt = m;
+    with_fused_shape(n, m, [&](auto nb, auto mb, auto exm) {
+      constexpr int NB = decltype(nb)::value, MB = decltype(mb)::value;
+      constexpr bool EXM = decltype(exm)::value;
+      const size_t smem = fused_smem_bytes<T, NB, MB>(q.K);
+      auto kern = q.K <= kHalfWarps ? k_fused_cta<T, NB, MB, 1, EXM> : k_fused_cta<T, NB, MB, 2, EXM>;
+      err = ensure_max_smem(kern, smem);
+      if (err == cudaSuccess) {
+        kern<<<grid, kThreads, smem, st>>>(q);
+        err = cudaGetLastError();
+      }
+      return true;
+    });
+    return err;
   } else {
     return cudaErrorNotSupported;
   }
@@ -1006,7 +915,7 @@ template size_t fused_slot_elems<double>(int, int, int, bool);
 template size_t fused_slot_elems<float>(int, int, int, bool);
 template bool fused_supported_dz<double>(int, int, int, int);
 template bool fused_supported_dz<float>(int, int, int, int);
-template cudaError_t launch_fused<double>(const FusedParams<double>&, int, cudaStream_t);
-template cudaError_t launch_fused<float>(const FusedParams<float>&, int, cudaStream_t);
+template cudaError_t launch_fused<double>(const FusedParams<double>&, int, int, int, cudaStream_t);
+template cudaError_t launch_fused<float>(const FusedParams<float>&, int, int, int, cudaStream_t);
 
 }  // namespace b2p

@@ -87,12 +87,15 @@ struct FusedParams {
   // dz = [x_0, u_0, ..., x_N] ([B][K n + N m]) from the formation's Q_k^-1 /
   // R_k^-1 (reconstruct_primal, kkt.cpp:153-181)
   T* dz_out;
+  int m_rt;  // control dimension (kernels compiled for a padded m read the real one here)
 };
 template <class T> bool fused_supported(int K, int n, int m, int kind);
 // shared memory / slot need grows with dz_out (Q_k^-1 kept for the finish)
 template <class T> bool fused_supported_dz(int K, int n, int m, int kind);
 template <class T> size_t fused_slot_elems(int K, int n, int m, bool keep_q = false);
-template <class T> cudaError_t launch_fused(const FusedParams<T>& p, int grid, cudaStream_t st);
+// one-CTA kernel shapes: (14, 7) and even n in [10, 16] with m <= 8
+template <class T>
+cudaError_t launch_fused(const FusedParams<T>& p, int n, int m, int grid, cudaStream_t st);
 
 // Fused one-CTA kernel for small blocks (small_kernels.cu): n, m <= 8 padded
 // to powers of two, everything in shared memory (the SQP / NMPC shapes).

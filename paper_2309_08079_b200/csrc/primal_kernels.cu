@@ -108,8 +108,21 @@ __device__ __forceinline__ void hw_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l, u
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     T s = a[k];
+    // Lt[k][q] = L(k,q) d_q: row k read as broadcast 16-byte pairs when rows
+    // are 16-byte aligned (fewer L1 instructions: the kernel is L1-issue-bound),
+    // same subtraction order
+    if constexpr (sizeof(T) == 8 && D % 2 == 0) {
 #pragma unroll
-    for (int q = 0; q < k; ++q) s -= a[q] * Lt[k * D + q];  // Lt[k][q] = L(k,q) d_q
+      for (int q = 0; q + 1 < k; q += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(Lt + k * D + q);
+        s -= a[q] * v.x;
+        s -= a[q + 1] * v.y;
+      }
+      if (k & 1) s -= a[k - 1] * Lt[k * D + k - 1];
+    } else {
+#pragma unroll
+      for (int q = 0; q < k; ++q) s -= a[q] * Lt[k * D + q];
+    }
     const T dk = __shfl_sync(mk, s, k, 16);
     const T rk = T(1) / dk;
     if (l == k) dl = dk;
@@ -173,18 +186,42 @@ __global__ void __launch_bounds__(16 * kPrHw) k_reconstruct_primal_hw(PrimalPara
     const int lr = l < NB ? l : NB - 1;
     // Q_k through the tile with coalesced 16-lane loads (each sector fetched once)
     const T* Q = p.Q + (static_cast<size_t>(sys) * K + k) * NB * NB;
-#pragma unroll
-    for (int i = l; i < NB * NB; i += 16) Lt[i] = __ldg(Q + i);
-    __syncwarp(mk);
+    constexpr bool kVec = sizeof(T) == 8 && NB % 2 == 0;  // 16-byte blocks and rows
     T a[NB];
+    if constexpr (kVec) {
+      // 16-byte coalesced loads / stores (every block and row starts 16-byte aligned)
 #pragma unroll
-    for (int j = 0; j < NB; ++j) a[j] = Lt[lr * NB + j];
+      for (int i = l; i < NB * NB / 2; i += 16)
+        reinterpret_cast<double2*>(Lt)[i] = __ldg(reinterpret_cast<const double2*>(Q) + i);
+      __syncwarp(mk);
+#pragma unroll
+      for (int j = 0; j < NB; j += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(Lt + lr * NB + j);
+        a[j] = v.x;
+        a[j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = l; i < NB * NB; i += 16) Lt[i] = __ldg(Q + i);
+      __syncwarp(mk);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) a[j] = Lt[lr * NB + j];
+    }
     __syncwarp(mk);
     T at = T(0);
     if (k < N) {  // (A_k' lambda_{k+1})_l = sum_j A_k(j, l) lambda_{k+1, j}
       const T* A = p.A + (static_cast<size_t>(sys) * N + k) * NB * NB;
+      if constexpr (kVec) {
 #pragma unroll
-      for (int j = 0; j < NB; ++j) at += __ldg(A + j * NB + lr) * __ldg(lam1 + j);
+        for (int j = 0; j < NB; j += 2) {
+          const double2 lv = __ldg(reinterpret_cast<const double2*>(lam1 + j));
+          at += __ldg(A + j * NB + lr) * lv.x;
+          at += __ldg(A + (j + 1) * NB + lr) * lv.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) at += __ldg(A + j * NB + lr) * __ldg(lam1 + j);
+      }
     }
     T rhs = -(__ldg(p.q + (static_cast<size_t>(sys) * K + k) * NB + lr) +
               __ldg(lam + static_cast<size_t>(k) * NB + lr) - at);
@@ -202,8 +239,17 @@ __global__ void __launch_bounds__(16 * kPrHw) k_reconstruct_primal_hw(PrimalPara
     __syncwarp(mk);
     const T* Bm = p.B_ + (static_cast<size_t>(sys) * N + k) * NB * MB;
     T bt = T(0);
+    if constexpr (sizeof(T) == 8 && NB % 2 == 0) {
 #pragma unroll
-    for (int j = 0; j < NB; ++j) bt += __ldg(Bm + j * MB + lr) * __ldg(lam1 + j);
+      for (int j = 0; j < NB; j += 2) {
+        const double2 lv = __ldg(reinterpret_cast<const double2*>(lam1 + j));
+        bt += __ldg(Bm + j * MB + lr) * lv.x;
+        bt += __ldg(Bm + (j + 1) * MB + lr) * lv.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) bt += __ldg(Bm + j * MB + lr) * __ldg(lam1 + j);
+    }
     T rhs = -(__ldg(p.r + (static_cast<size_t>(sys) * N + k) * MB + lr) - bt);
     hw_ldlt_solve<T, MB>(a, rhs, Lt, l, mk);
     if (l < MB) dz[NB + l] = rhs;
