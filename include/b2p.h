@@ -138,7 +138,8 @@ long long b2p_ctx_kernel_launches(b2p_ctx* ctx);
  * one-CTA kernel (n, m <= 8 fp64). */
 int b2p_ctx_last_path(b2p_ctx* ctx);
 /* Debug (B2P_PHASE_TIMING=1): per-system %globaltimer stamps of the last
- * one-CTA fused solve, [n][8] = start, F1 end, F2 end, staging end, end (ns).
+ * one-CTA fused solve, [n][16] = start, F1 end, F2 end, staging end, end (ns),
+ * then kernel-specific SM-clock segment sums (scripts/phase_probe.py).
  * Returns the number of systems copied. */
 int b2p_ctx_phase_stamps(b2p_ctx* ctx, unsigned long long* out, int n);
 

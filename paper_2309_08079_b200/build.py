@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libb2p.so")
 SOURCES = ["b2p_api.cu", "schur_kernels.cu", "pcg_kernels.cu", "fused_kernels.cu", "fc_kernels.cu", "fg_kernels.cu", "primal_kernels.cu", "small_kernels.cu"]
-HEADERS = ["common.cuh", "kernels.h", "warp_dense.cuh", "hw_dense.cuh", "wp_dense.cuh"]
+HEADERS = ["common.cuh", "kernels.h", "warp_dense.cuh", "hw_dense.cuh", "wp_dense.cuh", "tmem.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -37,9 +37,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         common += ["-Xptxas", "-v"]
     objs = []
     procs = []
+    hdeps = [os.path.join(CSRC, f) for f in HEADERS + ["tmem.cuh"]] + [os.path.join(inc, "b2p.h")]
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
+        if not force and not verbose and not _stale(obj, [os.path.join(CSRC, src)] + hdeps):
+            continue  # object up to date (per-file incremental rebuild)
         cmd = [NVCC] + common + ["-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     failed = False

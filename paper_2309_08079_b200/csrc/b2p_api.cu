@@ -574,7 +574,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       CK(cudaEventRecord(c->ev2, st));
     }
     f.timing = env_int("B2P_PHASE_TIMING", 0)
-                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
+                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 128ull * B))
                    : nullptr;
     c->timing = f.timing;
     c->timing_n = f.timing ? B : 0;
@@ -665,7 +665,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.slot = static_cast<T*>(ws_get(
         c, tag + "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, n, k->m, dz_dev != nullptr)));
     f.timing = env_int("B2P_PHASE_TIMING", 0)
-                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
+                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 128ull * B))
                    : nullptr;
     c->timing = f.timing;
     c->timing_n = f.timing ? B : 0;
@@ -745,7 +745,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       CK(cudaEventRecord(c->ev2, st));
     }
     f.timing = env_int("B2P_PHASE_TIMING", 0)
-                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 64ull * B))
+                   ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 128ull * B))
                    : nullptr;
     c->timing = f.timing;
     c->timing_n = f.timing ? B : 0;
@@ -1010,7 +1010,7 @@ int b2p_ctx_phase_stamps(b2p_ctx* c, unsigned long long* out, int n) {
   if (!c || !out || !c->timing) return B2P_INVALID_ARGUMENT;
   cudaSetDevice(c->device);
   const int m = std::min(n, c->timing_n);
-  if (cudaMemcpy(out, c->timing, sizeof(unsigned long long) * 8 * m, cudaMemcpyDeviceToHost) !=
+  if (cudaMemcpy(out, c->timing, sizeof(unsigned long long) * 16 * m, cudaMemcpyDeviceToHost) !=
       cudaSuccess)
     return B2P_CUDA_ERROR;
   return m;

@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(32 * (FgMaxRp<T, NB>::v + 1), 1)
     return t;
   };
   for (int sys = 0; sys < p.B; ++sys) {
-    unsigned long long* tm = (p.timing && c == 0 && tid == 0) ? p.timing + static_cast<size_t>(sys) * 8 : nullptr;
+    unsigned long long* tm = (p.timing && c == 0 && tid == 0) ? p.timing + static_cast<size_t>(sys) * 16 : nullptr;
     if (tm) {
       tm[0] = stamp();
       tm[5] = tm[6] = tm[7] = 0;

@@ -84,6 +84,22 @@ __device__ __forceinline__ void tma_copy_1d(void* dst_smem, const void* src, uns
       "l"(src), "r"(bytes), "r"(mbar_addr)
       : "memory");
 }
+// mbar_wait on the parity held in bit `bit` of st, which is then flipped
+__device__ __forceinline__ unsigned mbar_wait_bit(unsigned mbar_addr, unsigned& st, unsigned bit) {
+  unsigned done = 0, spins = 0;
+  const unsigned phase = (st & bit) ? 1u : 0u;
+  while (!done) {
+    ++spins;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
+        "1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(mbar_addr), "r"(phase)
+        : "memory");
+  }
+  st ^= bit;
+  return spins;
+}
 __device__ __forceinline__ void mbar_wait(unsigned mbar_addr, unsigned& phase) {
   unsigned done = 0;
   while (!done) {
@@ -147,9 +163,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   // its formation while this system's PCG runs (as are its q_k, into the q
   // region past `red`); sL: the L blocks at the padded stride LS.
   constexpr int LS = fused_ls(NB);
-  T* sD = smem;                                 // [K][NB][NB]
-  T* sL = smem + static_cast<size_t>(K) * NN;   // [K][LS]    (column products)
-  T* sp = sL + static_cast<size_t>(K) * LS;     // [K][NB]
+  T* sL = smem;                                 // [K][LS]  staging only
+  T* sD = smem + static_cast<size_t>(K) * LS;   // [K][NB][NB]  D row products
+  T* sp = sD + static_cast<size_t>(K) * NN;     // [K][NB]
   T* st = sp + K * NB;
   T* su = st + K * NB;
   T* red = su + K * NB;                  // [64]
@@ -162,8 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   __shared__ __align__(8) unsigned long long s_mbar2;  // next system's Q prefetch
   const unsigned mbar_addr = static_cast<unsigned>(__cvta_generic_to_shared(&s_mbar));
   const unsigned mbar2_addr = static_cast<unsigned>(__cvta_generic_to_shared(&s_mbar2));
-  unsigned mbar_phase = 0, mbar2_phase = 0;
-  bool qpre = false;  // this system's Q_k / q_k already on their way (prefetched)
+  // mbarrier phase parities and the prefetch flag packed in one register
+  // (bit 0: s_mbar, bit 1: s_mbar2, bit 2: this system's Q_k / q_k already on
+  // their way): loop-carried scalars that would otherwise be spilled
+  unsigned mst = 0;
   __shared__ unsigned s_taddr;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mbar_addr) : "memory");
@@ -180,8 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const unsigned tbase = s_taddr + ((32u * ((tid >> 5) & 3)) << 16) + 128u * (tid >> 7);
-  auto colD = [&](int r) { return tbase + 32u * r; };
-  auto colL = [&](int r) { return tbase + 64u + 32u * r; };
+  auto colR = [&](int r) { return tbase + 32u * r; };        // R_b = L_{b+1}' rows
+  auto colL = [&](int r) { return tbase + 64u + 32u * r; };  // L_b rows
   // CTA-private slot (L2 resident): L and D (TMA-staged for the PCG phase),
   // theta^-1, gamma, R^-1
   const bool keep_q = p.dz_out != nullptr;
@@ -206,8 +224,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     const T* x0 = p.x0 + static_cast<size_t>(sys) * NB;
 
     __syncthreads();  // previous system's PCG is done with shared memory
-    unsigned long long* tm = (p.timing && tid == 0) ? p.timing + static_cast<size_t>(sys) * 8 : nullptr;
+    unsigned long long* tm = (p.timing && tid == 0) ? p.timing + static_cast<size_t>(sys) * 16 : nullptr;
     if (tm) tm[0] = gtimer();
+    if (tm) tm[13] = gtimer();
     if (tid == 0) s_err = 0x7fffffff;
 
     T* hw = smem + FL::ohw(K) + static_cast<size_t>(h) * FL::per_hw;
@@ -224,8 +243,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // row, schur.cpp:49-51; same arithmetic). All Q_k arrive in one TMA bulk
     // copy (sQi) and are inverted in place; lanes read their rows from smem.
     T* sq = smem + FL::osq(K);  // q_k of every knot (for Q_k^-1 q_k)
-    if (qpre) {
-      mbar_wait(mbar2_addr, mbar2_phase);  // prefetched during the previous PCG
+    if (tm) tm[14] = gtimer();
+    if (mst & 4u) {
+      const unsigned mst0 = mst;
+      const unsigned sp_ = mbar_wait_bit(mbar2_addr, mst, 2u);  // prefetched during the previous PCG
+      if (tm) tm[15] = sp_ + (static_cast<unsigned long long>(mst0) << 32);
     } else {
       if (tid == 0) {
         const unsigned bq = static_cast<unsigned>(sizeof(T) * K * nn);
@@ -237,9 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         tma_copy_1d(sQi, Qs, bq, mbar_addr);
         tma_copy_1d(sq, qs, bv, mbar_addr);
       }
-      mbar_wait(mbar_addr, mbar_phase);
+      mbar_wait_bit(mbar_addr, mst, 1u);
     }
-    qpre = false;
+    mst &= ~4u;
+    if (tm) tm[11] = gtimer();
     // Both half-warps of a warp always run the same code (out-of-range knots
     // recompute a clamped duplicate and store nothing), so every shuffle and
     // sync below uses the full-warp mask.
@@ -285,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           sqq[k * 16 + l] = qq;
         }
       }
+      if (tm) tm[8 + r] = gtimer();
     }
     {
       // R_k^-1 of the half-warp's two knots at once (m = 7 fits 8-lane groups):
@@ -312,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         srr[k * 8 + ls] = rr;
       }
     }
+    if (tm) tm[10] = gtimer();
     __syncthreads();
 
     if (tm) tm[1] = gtimer();
@@ -535,19 +560,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       lam[c] = (pact && p.lambda0) ? p.lambda0[static_cast<size_t>(sys) * K * NB + pbc * NB + row]
                                    : T(0);
     }
-    mbar_wait(mbar_addr, mbar_phase);
+    mbar_wait_bit(mbar_addr, mst, 1u);
     {
       T mrow[NB];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const T* Dr = sD + static_cast<size_t>(pbc) * NN + (pr + H * c) * NB;
+        // row pr + H c of R_b = column pr + H c of L_{b+1} (padded stride LS:
+        // the four quarter-warps read disjoint banks)
+        const T* Lc = sL + static_cast<size_t>(pbn) * LS + pr + H * c;
 #pragma unroll
-        for (int j = 0; j < NB; j += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(Dr + j);
-          mrow[j] = v.x;
-          mrow[j + 1] = v.y;
-        }
-        tm::st_row<NB>(colD(c), mrow);
+        for (int j = 0; j < NB; ++j) mrow[j] = Lc[j * NB];
+        tm::st_row<NB>(colR(c), mrow);
         const T* Lr = sL + static_cast<size_t>(pbc) * LS + (pr + H * c) * NB;
 #pragma unroll
         for (int j = 0; j < NB; j += 2) {
@@ -562,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
     for (int c = 0; c < 2; ++c)
       if (pact) sp[pbc * NB + pi + H * c] = lam[c];
-    __syncthreads();  // sD consumed: the next system's Q may land in [0, K*NN)
+    __syncthreads();  // sL consumed: the next system's Q may land in [0, K*NN)
     if (tm) tm[3] = gtimer();
     {
       const int nsys = sys + gridDim.x;
@@ -577,17 +600,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           tma_copy_1d(sQi, p.Q + static_cast<size_t>(nsys) * K * nn, bq, mbar2_addr);
           tma_copy_1d(smem + FL::osq(K), p.q + static_cast<size_t>(nsys) * K * NB, bv, mbar2_addr);
         }
-        qpre = true;
+        mst |= 4u;
       }
       if (nsys < p.B && tid < 9) {
         // per-field contiguous ranges of the next system (16-byte aligned inside)
-        const T* base[9] = {p.Q, p.q, p.R, p.r, p.A, p.Bm, p.e, p.x_s, p.x0};
-        const size_t per[9] = {static_cast<size_t>(K) * NN, static_cast<size_t>(K) * NB,
-                               static_cast<size_t>(N) * m * m, static_cast<size_t>(N) * m,
-                               static_cast<size_t>(N) * NN, static_cast<size_t>(N) * NB * m,
-                               static_cast<size_t>(N) * NB, NB, NB};
-        const char* lo = reinterpret_cast<const char*>(base[tid] + nsys * per[tid]);
-        const char* hi = lo + per[tid] * sizeof(T);
+        // (a switch, not an indexed array: no local-memory copy of the table)
+        const T* base;
+        size_t per;
+        switch (tid) {
+          case 0: base = p.Q; per = static_cast<size_t>(K) * NN; break;
+          case 1: base = p.q; per = static_cast<size_t>(K) * NB; break;
+          case 2: base = p.R; per = static_cast<size_t>(N) * m * m; break;
+          case 3: base = p.r; per = static_cast<size_t>(N) * m; break;
+          case 4: base = p.A; per = static_cast<size_t>(N) * NN; break;
+          case 5: base = p.Bm; per = static_cast<size_t>(N) * NB * m; break;
+          case 6: base = p.e; per = static_cast<size_t>(N) * NB; break;
+          case 7: base = p.x_s; per = NB; break;
+          default: base = p.x0; per = NB; break;
+        }
+        const char* lo = reinterpret_cast<const char*>(base + nsys * per);
+        const char* hi = lo + per * sizeof(T);
         const char* a = reinterpret_cast<const char*>((reinterpret_cast<uintptr_t>(lo) + 15) & ~uintptr_t(15));
         const char* e = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(hi) & ~uintptr_t(15));
         if (e > a)
@@ -602,9 +634,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // on in-bounds shared memory and discarded by the selects.
     auto Srows = [&](const T* x, T (&y)[2]) {
       T sd[2], sl[2], sr[2];
-      tm::dot2_row<NB>(colD(0), colD(1), x + pbc * NB, sd[0], sd[1]);  // D_b rows (TMEM)
+      dots_row2<T, NB>(sD + static_cast<size_t>(pbc) * NN + pr * NB, x + pbc * NB, sd);  // D_b rows (smem)
       tm::dot2_row<NB>(colL(0), colL(1), x + pbl * NB, sl[0], sl[1]);  // L_b rows (TMEM)
-      dots_col2<T, NB, LS>(sL + static_cast<size_t>(pbn) * LS + pr, x + pbn * NB, sr);
+      tm::dot2_row<NB>(colR(0), colR(1), x + pbn * NB, sr[0], sr[1]);  // R_b rows (TMEM)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         T out = sd[c];
@@ -653,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       // u = r - L_b t_{b-1} - R_b t_{b+1}
       T sl[2], sr[2];
       tm::dot2_row<NB>(colL(0), colL(1), st + pbl * NB, sl[0], sl[1]);
-      dots_col2<T, NB, LS>(sL + static_cast<size_t>(pbn) * LS + pr, st + pbn * NB, sr);
+      tm::dot2_row<NB>(colR(0), colR(1), st + pbn * NB, sr[0], sr[1]);
       __syncwarp();  // every lane has read its block's r from su
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -692,13 +724,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       for (int c = 0; c < 2; ++c)
         if (pact) sp[pbc * NB + pi + H * c] = pp[c];
       __syncthreads();
+      // B2P_PHASE_TIMING: per-segment SM-clock sums of thread 0 over the
+      // iterations (Srows | upsilon reduce | update + precondition | eta
+      // reduce | beta + p + barrier), packed two per stamp slot 5..7
+      unsigned seg[5] = {0, 0, 0, 0, 0}, c0 = tm ? static_cast<unsigned>(clock()) : 0u;
+      auto segmark = [&](int i) {
+        if (tm) {
+          const unsigned c1 = static_cast<unsigned>(clock());
+          seg[i] += c1 - c0;
+          c0 = c1;
+        }
+      };
       for (int it = 1; it <= p.max_iter; ++it) {
         T up = T(0);
         Srows(sp, spv);
 #pragma unroll
         for (int c = 0; c < 2; ++c)
           if (pact) up += pp[c] * spv[c];
+        segmark(0);
         const T ups = block_reduce(up, red + 32);  // buffer B
+        segmark(1);
         if (!is_finite(ups)) {
           code = kRuntime;
           which = kWhichUpsNonFinite;
@@ -723,7 +768,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
         for (int c = 0; c < 2; ++c)
           if (pact) ep += rr[c] * rt[c];
+        segmark(2);
         const T eta_p = block_reduce(ep, red);
+        segmark(3);
         if (!is_finite(eta_p)) {
           code = kRuntime;
           which = kWhichEtaNonFinite;
@@ -751,6 +798,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         }
         eta = eta_p;
         __syncthreads();
+        segmark(4);
+      }
+      if (tm) {
+        tm[5] = seg[0] | (static_cast<unsigned long long>(seg[1]) << 32);
+        tm[6] = seg[2] | (static_cast<unsigned long long>(seg[3]) << 32);
+        tm[7] = seg[4];
       }
     }
     if (code == kOk) {
@@ -766,10 +819,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       // half-warp h takes knots h, h + 32, lane i = row i,
       //   dx_k = Q_k^-1 (-((q_k + lambda_k) - A_k' lambda_{k+1})),
       //   du_k = R_k^-1 (-(r_k - B_k' lambda_{k+1})), dx_N = Q_N^-1 (-(q_N + lambda_N)).
-      __syncthreads();  // lambda (global) complete; sL is dead
+      __syncthreads();  // lambda (global) complete; sD is dead (sL may hold the next Q)
       const T* lamo = p.lambda_out + static_cast<size_t>(sys) * K * NB;
       T* dz = p.dz_out + static_cast<size_t>(sys) * (static_cast<size_t>(K) * NB + static_cast<size_t>(N) * m);
-      T* W = sL + h * 32;  // this half-warp's right-hand sides
+      T* W = sD + h * 32;  // this half-warp's right-hand sides
 #pragma unroll 1
       for (int r = 0; r < R; ++r) {
         const int k = h + r * kHalfWarps;
@@ -806,6 +859,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         }
         __syncwarp();
       }
+    }
+    if (tm && (mst & 4u)) {  // debug: has the next system's Q prefetch landed by now?
+      unsigned done;
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
+          "1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(mbar2_addr), "r"((mst >> 1) & 1u)
+          : "memory");
+      unsigned done2;
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
+          "1, 0, p;\n}\n"
+          : "=r"(done2)
+          : "r"(mbar2_addr), "r"(((mst >> 1) & 1u) ^ 1u)
+          : "memory");
+      tm[12] = done + 2 * done2 + 4 * mst;
     }
     if (tid == 0) {
       SysOut o;

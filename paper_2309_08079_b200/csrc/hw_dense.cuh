@@ -200,6 +200,26 @@ __device__ __forceinline__ void dots_col2(const T* Mc, const T* x, T (&out)[2]) 
   out[0] = a0 + c0;
   out[1] = a1 + c1;
 }
+// Two rows (pr, pr + NB/2) of one row-major shared block per thread (M = block
+// + pr NB) against one broadcast vector x: 16-byte pair loads, the same
+// two-accumulator order (even j -> a, odd j -> c) as tm::dot2_row.
+template <class T, int NB>
+__device__ __forceinline__ void dots_row2(const T* M, const T* x, T (&out)[2]) {
+  constexpr int H = NB / 2;
+  T a0 = T(0), c0 = T(0), a1 = T(0), c1 = T(0);
+#pragma unroll
+  for (int j = 0; j < NB; j += 2) {
+    const double2 v2 = *reinterpret_cast<const double2*>(x + j);
+    const double2 m0 = *reinterpret_cast<const double2*>(M + j);
+    const double2 m1 = *reinterpret_cast<const double2*>(M + H * NB + j);
+    a0 += m0.x * v2.x;
+    c0 += m0.y * v2.y;
+    a1 += m1.x * v2.x;
+    c1 += m1.y * v2.y;
+  }
+  out[0] = a0 + c0;
+  out[1] = a1 + c1;
+}
 // out[c] = ti[c] . v for two register rows against one shared vector
 template <class T, int NB>
 __device__ __forceinline__ void dots_reg2(const T (&ti)[2][NB], const T* v, T (&out)[2]) {

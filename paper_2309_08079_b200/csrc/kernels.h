@@ -75,7 +75,7 @@ struct FusedParams {
   int trace_cap;
   double epsilon;
   int max_iter;
-  unsigned long long* timing;  // optional [B][8] globaltimer stamps per phase (debug)
+  unsigned long long* timing;  // optional [B][16] globaltimer stamps per phase (debug)
   // formation only (build_schur): write S [B][K][3][n][n] (zeroed pads), gamma
   // [B][K n], theta^-1 [B][K][n][n] in the reference layout and skip the PCG
   T* S_out;

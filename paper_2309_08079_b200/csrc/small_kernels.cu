@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kSmallThreads, (!BATCH ? 1 : (NP <= 2 ? 4 : (N
 
   for (int sys = blockIdx.x; sys < p.B; sys += gridDim.x) {
     __syncthreads();  // previous system done with shared memory
-    unsigned long long* tm = (p.timing && tid == 0) ? p.timing + size_t(sys) * 8 : nullptr;
+    unsigned long long* tm = (p.timing && tid == 0) ? p.timing + size_t(sys) * 16 : nullptr;
     if (tm) tm[0] = small_gtimer();
     // Stage the system's knot data (the b2p_kkt layout, unpadded) in shared
     // memory with coalesced cp.async copies, all issued before any is consumed: the

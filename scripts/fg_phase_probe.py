@@ -15,7 +15,7 @@ for name, (seed, N, n, m, dt, eps) in cases.items():
     kkt = api.random_kkt(seed, N, n, m)
     for _ in range(3):
         r = api.solve(kkt, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=eps), dtype=dt)
-    buf = np.zeros((1, 8), dtype=np.uint64)
+    buf = np.zeros((1, 16), dtype=np.uint64)
     load().b2p_ctx_phase_stamps(api.context().handle, buf.ctypes.data, 1)
     t = buf[0].astype(np.int64)
     it = r.report.iterations

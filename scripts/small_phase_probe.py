@@ -16,7 +16,7 @@ for (N, n, m) in [(32, 2, 1), (32, 4, 1), (128, 4, 1)]:
     rows = []
     for _ in range(10):
         r = api.solve(kkt, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
-        buf = np.zeros((1, 8), dtype=np.uint64)
+        buf = np.zeros((1, 16), dtype=np.uint64)
         load().b2p_ctx_phase_stamps(api.context().handle, buf.ctypes.data, 1)
         rows.append(np.diff(buf[0, :5].astype(np.int64)) / 1e3)
     d = np.median(np.array(rows[3:]), axis=0)
