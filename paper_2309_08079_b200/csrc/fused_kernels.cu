@@ -44,11 +44,15 @@ struct FLayout {
   // tW: transposes / AQ / Lr tile; tX: L^-T tile, aliased by B R^-1; rd[16], v[16]
   static constexpr int TX = NB * NB > 128 ? NB * NB : 128;  // >= two 8x8 R^-1 tiles
   static constexpr int per_hw = NB * LD + TX + 32;
+  // 8-lane group tiles of F1 (L^-T of Q_g, then the R_g^-1 tiles) and of the
+  // theta^-1 pass: [max(n n, 2 MB MB)] | rd [16]
+  static constexpr int g8_tile = (NB * NB > 2 * MB * MB ? NB * NB : 2 * MB * MB) + 16;
+  static constexpr int tiles = kHalfWarps * per_hw > 64 * g8_tile ? kHalfWarps * per_hw : 64 * g8_tile;
   __host__ __device__ static int oQi(int) { return 0; }
   __host__ __device__ static int oqq(int K) { return K * NB * NB; }
   __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
   __host__ __device__ static int ohw(int K) { return orr(K) + (K - 1) * 8; }
-  __host__ __device__ static int osq(int K) { return ohw(K) + kHalfWarps * per_hw; }  // q_k
+  __host__ __device__ static int osq(int K) { return ohw(K) + tiles; }  // q_k
   __host__ __device__ static int total(int K) { return osq(K) + K * NB; }
 };
 
@@ -85,20 +89,18 @@ __device__ __forceinline__ void tma_copy_1d(void* dst_smem, const void* src, uns
       : "memory");
 }
 // mbar_wait on the parity held in bit `bit` of st, which is then flipped
-__device__ __forceinline__ unsigned mbar_wait_bit(unsigned mbar_addr, unsigned& st, unsigned bit) {
-  unsigned done = 0, spins = 0;
+__device__ __forceinline__ void mbar_wait_bit(unsigned mbar_addr, unsigned& st, unsigned bit) {
+  unsigned done = 0;
   const unsigned phase = (st & bit) ? 1u : 0u;
   while (!done) {
-    ++spins;
     asm volatile(
-        "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
         "1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(mbar_addr), "r"(phase)
         : "memory");
   }
   st ^= bit;
-  return spins;
 }
 __device__ __forceinline__ void mbar_wait(unsigned mbar_addr, unsigned& phase) {
   unsigned done = 0;
@@ -226,7 +228,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     __syncthreads();  // previous system's PCG is done with shared memory
     unsigned long long* tm = (p.timing && tid == 0) ? p.timing + static_cast<size_t>(sys) * 16 : nullptr;
     if (tm) tm[0] = gtimer();
-    if (tm) tm[13] = gtimer();
     if (tid == 0) s_err = 0x7fffffff;
 
     T* hw = smem + FL::ohw(K) + static_cast<size_t>(h) * FL::per_hw;
@@ -243,11 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // row, schur.cpp:49-51; same arithmetic). All Q_k arrive in one TMA bulk
     // copy (sQi) and are inverted in place; lanes read their rows from smem.
     T* sq = smem + FL::osq(K);  // q_k of every knot (for Q_k^-1 q_k)
-    if (tm) tm[14] = gtimer();
     if (mst & 4u) {
-      const unsigned mst0 = mst;
-      const unsigned sp_ = mbar_wait_bit(mbar2_addr, mst, 2u);  // prefetched during the previous PCG
-      if (tm) tm[15] = sp_ + (static_cast<unsigned long long>(mst0) << 32);
+      mbar_wait_bit(mbar2_addr, mst, 2u);  // prefetched during the previous PCG
     } else {
       if (tid == 0) {
         const unsigned bq = static_cast<unsigned>(sizeof(T) * K * nn);
@@ -263,80 +261,92 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     }
     mst &= ~4u;
     if (tm) tm[11] = gtimer();
-    // Both half-warps of a warp always run the same code (out-of-range knots
-    // recompute a clamped duplicate and store nothing), so every shuffle and
-    // sync below uses the full-warp mask.
-#pragma unroll 1
-    for (int r = 0; r < R; ++r) {
-      const int k = h + r * kHalfWarps;
-      // R_k row l issued before the Q_k inverse so its L2 latency is hidden
+    // 8-lane group g = tid / 8 inverts Q_g (lane gl < n/2 owns rows gl and
+    // gl + n/2: every broadcast tile operand serves two rows) and then R_g,
+    // all 64 knots in one pass. Groups past the horizon recompute a clamped
+    // duplicate in their own tile and store nothing, so every shuffle and sync
+    // is full-warp.
+    {
+      constexpr int H = NB / 2;
+      const int g = tid >> 3, gl = tid & 7;
+      const int glr = gl < H ? gl : H - 1;
+      T* gt = smem + FL::ohw(K) + static_cast<size_t>(g) * FL::g8_tile;
+      const bool kv = g < K;
+      const int kc = kv ? g : K - 1;
+      // R_g row issued first: its L2 latency hides behind the Q_g inverse
+      const bool rv = g < N;
+      const int rc = rv ? g : N - 1;
+      const int lm = gl < MB ? gl : MB - 1;
+      T ra[MB];
       {
-        const bool kv = k < K;
-        const int kc = kv ? k : K - 1;
-        T a[NB], x[NB];
-        // clamped duplicates (k >= K) read Q_{K-1} from global memory: its
-        // shared-memory copy is being inverted in place by its owner
-        if (kv) {
-          const T* Qr = sQi + static_cast<size_t>(kc) * nn + lr * NB;
+        const T* Rr = Rs + static_cast<size_t>(rc) * m * m + lm * m;
 #pragma unroll
-          for (int i = 0; i < NB; i += 2) {
-            const double2 q2 = *reinterpret_cast<const double2*>(Qr + i);
-            a[i] = q2.x;
-            a[i + 1] = q2.y;
-          }
-        } else {
-          const T* Qr = Qs + static_cast<size_t>(kc) * nn + lr * NB;
+        for (int i = 0; i < MB; ++i)  // identity pad rows / columns past m
+          ra[i] = (EXM || (lm < m && i < m)) ? __ldg(Rr + i) : (lm == i ? T(1) : T(0));
+      }
+      T a0[NB], a1[NB], x0[NB], x1[NB];
+      // clamped duplicates read Q_{K-1} from global memory (its shared copy
+      // is inverted in place by its owner)
+      if (kv) {
+        const T* Q0 = sQi + static_cast<size_t>(kc) * nn + glr * NB;
 #pragma unroll
-          for (int i = 0; i < NB; i += 2) {
-            const double2 q2 = __ldg(reinterpret_cast<const double2*>(Qr + i));
-            a[i] = q2.x;
-            a[i + 1] = q2.y;
-          }
+        for (int i = 0; i < NB; i += 2) {
+          const double2 u = *reinterpret_cast<const double2*>(Q0 + i);
+          const double2 v = *reinterpret_cast<const double2*>(Q0 + H * NB + i);
+          a0[i] = u.x; a0[i + 1] = u.y; a1[i] = v.x; a1[i + 1] = v.y;
         }
-        const int f = hw_spd_inverse_v2<T, NB, true>(a, tW, tX, rd, l, x);
-        __syncwarp();  // every lane has consumed its Q_k row: overwrite in place
-        // first failing call in row order: row k as its Q_{k+1} (key 4k+2), or row 0
-        if (kv && f >= 0) fkey = min(fkey, k == 0 ? 0 : 4 * k + 2);
-        if (kv && lact) {
-          T qq = T(0);
+      } else {
+        const T* Q0 = Qs + static_cast<size_t>(kc) * nn + glr * NB;
 #pragma unroll
-          for (int i = 0; i < NB; ++i) {
-            sQi[k * NN + i * NB + l] = x[i];
-            qq += x[i] * sq[k * NB + i];
-            if (keep_q) gQ[static_cast<size_t>(k) * NN + i * NB + l] = x[i];
-          }
-          sqq[k * 16 + l] = qq;
+        for (int i = 0; i < NB; i += 2) {
+          const double2 u = __ldg(reinterpret_cast<const double2*>(Q0 + i));
+          const double2 v = __ldg(reinterpret_cast<const double2*>(Q0 + H * NB + i));
+          a0[i] = u.x; a0[i + 1] = u.y; a1[i] = v.x; a1[i + 1] = v.y;
         }
       }
-      if (tm) tm[8 + r] = gtimer();
-    }
-    {
-      // R_k^-1 of the half-warp's two knots at once (m = 7 fits 8-lane groups):
-      // lanes 0-7 knot h, lanes 8-15 knot h + 32
-      static_assert(MB <= 8, "");
-      const int sub = l >> 3, ls = l & 7;
-      const int k = h + sub * kHalfWarps;
-      const bool kv = k < N && sub < R;
-      const int kc = kv ? k : N - 1;
-      const int lm = ls < MB ? ls : MB - 1;
-      T ra[MB], x[MB];
-      const T* Rr = Rs + static_cast<size_t>(kc) * m * m + lm * m;
+      T* Lr = kv ? sQi + static_cast<size_t>(kc) * nn : gt;  // in place for owners
+      const int f = g8x2_spd_inverse<T, NB>(a0, a1, Lr, gt, gt + FL::g8_tile - 16, gl, x0, x1);
+      // first failing call in row order: row k as its Q_{k+1} (key 4k+2), or row 0
+      if (kv && f >= 0) fkey = min(fkey, g == 0 ? 0 : 4 * g + 2);
+      if (kv && gl < H) {
+        // Q_g^-1 rows (bitwise symmetric: = columns, which F2 reads)
+        T qq0 = T(0), qq1 = T(0);
+        T* X0 = sQi + static_cast<size_t>(g) * NN + glr * NB;
 #pragma unroll
-      for (int i = 0; i < MB; ++i)  // identity pad rows / columns past m
-        ra[i] = (EXM || (lm < m && i < m)) ? __ldg(Rr + i) : (lm == i ? T(1) : T(0));
-      const int f = g8_spd_inverse<T, MB>(ra, tW + sub * 64, tX + sub * 64, rd + sub * 8, ls, x);
-      if (kv && f >= 0) fkey = min(fkey, 4 * (k + 1) + 1);
-      if (kv && ls < MB) {
+        for (int i = 0; i < NB; i += 2) {
+          *reinterpret_cast<double2*>(X0 + i) = make_double2(x0[i], x0[i + 1]);
+          *reinterpret_cast<double2*>(X0 + H * NB + i) = make_double2(x1[i], x1[i + 1]);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const T qi = sq[g * NB + i];
+          qq0 += x0[i] * qi;
+          qq1 += x1[i] * qi;
+          if (keep_q) {
+            gQ[static_cast<size_t>(g) * NN + glr * NB + i] = x0[i];
+            gQ[static_cast<size_t>(g) * NN + (glr + H) * NB + i] = x1[i];
+          }
+        }
+        sqq[g * 16 + glr] = qq0;
+        sqq[g * 16 + glr + H] = qq1;
+      }
+      if (tm) tm[8] = gtimer();
+      // R_g^-1 (m <= 8 rows, one per lane) in the group's tile (its L^-T is dead)
+      static_assert(MB <= 8, "");
+      T xr[MB];
+      const int fr = g8_spd_inverse<T, MB>(ra, gt, gt + MB * MB, gt + FL::g8_tile - 16, gl, xr);
+      if (rv && fr >= 0) fkey = min(fkey, 4 * (g + 1) + 1);
+      if (rv && gl < MB) {
         T rr = T(0);
 #pragma unroll
         for (int i = 0; i < MB; ++i) {
-          gR[static_cast<size_t>(k) * mm + i * MB + ls] = x[i];
-          rr += x[i] * ((EXM || i < m) ? rs[k * m + i] : T(0));
+          gR[static_cast<size_t>(g) * mm + i * MB + gl] = xr[i];
+          rr += xr[i] * ((EXM || i < m) ? rs[g * m + i] : T(0));
         }
-        srr[k * 8 + ls] = rr;
+        srr[g * 8 + gl] = rr;
       }
+      if (tm) tm[9] = gtimer();
     }
-    if (tm) tm[10] = gtimer();
     __syncthreads();
 
     if (tm) tm[1] = gtimer();
@@ -351,8 +361,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       if (b0 == 0) {
         // schur.cpp:53-57: S(0,0) = Q0^-1, theta_inv[0] = sym(Q0), gamma_0
         if (lact) {
-#pragma unroll
-          for (int i = 0; i < NB; ++i) gT[i * NB + l] = T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
           gG[l] = -((xs[l] - x0[l]) + sqq[l]);
           if (p.form_only) {
             T* So = p.S_out + static_cast<size_t>(sys) * K * 3 * nn;
@@ -481,29 +489,64 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
             p.S_out[((static_cast<size_t>(sys) * K + bd) * 3 + 1) * nn + i * NB + l] = d;
         }
       }
-      // theta^-1 (schur.cpp:75): x holds row l of the symmetric theta
-      {
-        T th[NB];
-#pragma unroll
-        for (int i = 0; i < NB; ++i) th[i] = x[i];
-        const int f = hw_spd_inverse_v2<T, NB, true>(th, tW, tX, rd, l, x);
-        if (wr && f >= 0) fkey = min(fkey, b * 4 + 3);
-      }
+      // theta_b -> knot b-1's Q^-1 region for the theta^-1 pass: dead once every
+      // half-warp has finished this round (round 0: knots 0..30, round 1: 31..62)
+      __syncthreads();
       if (wr && lact) {
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          gT[static_cast<size_t>(b) * nn + i * NB + l] = x[i];
-          if (p.form_only)  // theta_inv[b] (bitwise symmetric: row = column)
-            p.theta_out[(static_cast<size_t>(sys) * K + b) * nn + i * NB + l] = x[i];
+        for (int i = 0; i < NB; ++i) sQi[(b - 1) * NN + i * NB + l] = x[i];
+      }
+    }
+    // ===================================================== theta^-1 (schur.cpp:75)
+    // One pass over all rows on 8-lane groups: group b = tid / 8, lane gl owns
+    // rows gl and gl + n/2 — exactly the PCG's quarter-warp mapping, so the
+    // inverse's output rows ARE the PCG thread's theta_b^-1 register rows
+    // (no slot round trip). theta_b is read from shared memory (F2 left it in
+    // knot b-1's region).
+    T ti[2][NB];
+    __syncthreads();  // every theta_b is in place; the formation tiles are free
+    if (tm) tm[10] = gtimer();
+    {
+      constexpr int H = NB / 2;
+      const int b = tid >> 3, gl = tid & 7;
+      const int glr = gl < H ? gl : H - 1;
+      // row 0 and rows past the horizon invert a clamped theta (row 1 / K-1)
+      // in their own tile and keep nothing: convergent full-warp syncs
+      const int bi = b == 0 ? 1 : (b < K ? b : K - 1);
+      T* gt = smem + FL::ohw(K) + static_cast<size_t>(b) * FL::g8_tile;
+      T a0[NB], a1[NB];
+      const T* Th = sQi + static_cast<size_t>(bi - 1) * nn + glr * NB;
+#pragma unroll
+      for (int i = 0; i < NB; i += 2) {
+        const double2 u = *reinterpret_cast<const double2*>(Th + i);
+        const double2 v = *reinterpret_cast<const double2*>(Th + H * NB + i);
+        a0[i] = u.x; a0[i + 1] = u.y; a1[i] = v.x; a1[i + 1] = v.y;
+      }
+      const int f = g8x2_spd_inverse<T, NB>(a0, a1, gt, gt, gt + FL::g8_tile - 16, gl, ti[0], ti[1]);
+      if (b >= 1 && b < K && f >= 0) fkey = min(fkey, b * 4 + 3);
+      if (b == 0) {  // theta_inv[0] = sym(Q_0), not an inverse (schur.cpp:55)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int row = glr + H * c;
+#pragma unroll
+          for (int j = 0; j < NB; ++j) ti[c][j] = T(0.5) * (Qs[row * NB + j] + Qs[j * NB + row]);
+        }
+      }
+      if (p.form_only && b >= 1 && b < K && gl < H) {  // theta_inv[b] rows
+        T* To = p.theta_out + (static_cast<size_t>(sys) * K + b) * nn;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          To[glr * NB + j] = ti[0][j];
+          To[(glr + H) * NB + j] = ti[1][j];
         }
       }
     }
-    // F2's global writes (L, D, theta^-1, gamma) are read back by the async
-    // proxy (TMA) below: order them before the barrier
+    // F2's global writes (L, D, gamma) are read back by the async proxy (TMA)
+    // below: order them before the barrier
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     if (tm) tm[2] = gtimer();
-    // the R^-1 pass runs two 8-lane groups per half-warp (knots h, h + 32): each
-    // group's first lane reports its own (group-uniform) failures
+    // every failure key is 8-lane-group uniform (F1, theta^-1): each group's
+    // first lane reports
     if ((l & 7) == 0 && fkey != 0x7fffffff) atomicMin(&s_err, fkey);
     __syncthreads();
     if (s_err != 0x7fffffff) {
@@ -548,14 +591,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         tma_copy_1d(sL, gL, bl, mbar_addr);
       }
     }
-    T ti[2][NB];
     T lam[2], rr[2], rt[2], pp[2], spv[2], best[2], gam[2];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int row = pr + H * c;
-      // theta^-1 row, stored transposed by F2 (bitwise symmetric)
-#pragma unroll
-      for (int j = 0; j < NB; ++j) ti[c][j] = __ldcg(gT + static_cast<size_t>(pbc) * NN + j * NB + row);
       gam[c] = __ldcg(gG + pbc * NB + row);
       lam[c] = (pact && p.lambda0) ? p.lambda0[static_cast<size_t>(sys) * K * NB + pbc * NB + row]
                                    : T(0);
@@ -727,12 +766,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       // B2P_PHASE_TIMING: per-segment SM-clock sums of thread 0 over the
       // iterations (Srows | upsilon reduce | update + precondition | eta
       // reduce | beta + p + barrier), packed two per stamp slot 5..7
-      unsigned seg[5] = {0, 0, 0, 0, 0}, c0 = tm ? static_cast<unsigned>(clock()) : 0u;
+      // (sums in shared memory: no registers or local memory in the solve path)
+      __shared__ unsigned s_seg[6];
+      if (tm) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) s_seg[i] = 0u;
+        s_seg[5] = static_cast<unsigned>(clock());
+      }
       auto segmark = [&](int i) {
         if (tm) {
           const unsigned c1 = static_cast<unsigned>(clock());
-          seg[i] += c1 - c0;
-          c0 = c1;
+          s_seg[i] += c1 - s_seg[5];
+          s_seg[5] = c1;
         }
       };
       for (int it = 1; it <= p.max_iter; ++it) {
@@ -801,9 +846,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         segmark(4);
       }
       if (tm) {
-        tm[5] = seg[0] | (static_cast<unsigned long long>(seg[1]) << 32);
-        tm[6] = seg[2] | (static_cast<unsigned long long>(seg[3]) << 32);
-        tm[7] = seg[4];
+        tm[5] = s_seg[0] | (static_cast<unsigned long long>(s_seg[1]) << 32);
+        tm[6] = s_seg[2] | (static_cast<unsigned long long>(s_seg[3]) << 32);
+        tm[7] = s_seg[4];
       }
     }
     if (code == kOk) {
@@ -859,23 +904,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         }
         __syncwarp();
       }
-    }
-    if (tm && (mst & 4u)) {  // debug: has the next system's Q prefetch landed by now?
-      unsigned done;
-      asm volatile(
-          "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
-          "1, 0, p;\n}\n"
-          : "=r"(done)
-          : "r"(mbar2_addr), "r"((mst >> 1) & 1u)
-          : "memory");
-      unsigned done2;
-      asm volatile(
-          "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, "
-          "1, 0, p;\n}\n"
-          : "=r"(done2)
-          : "r"(mbar2_addr), "r"(((mst >> 1) & 1u) ^ 1u)
-          : "memory");
-      tm[12] = done + 2 * done2 + 4 * mst;
     }
     if (tid == 0) {
       SysOut o;

@@ -324,6 +324,99 @@ __device__ __forceinline__ int hw_spd_inverse_v2(T (&a)[N], T* Lr, T* LiT, T* rd
 }
 
 
+// hw_spd_inverse_v2 on an 8-lane group with two rows per lane: lane l < H =
+// N / 2 owns rows l and l + H (lanes >= H duplicate rows H - 1, N - 1 and
+// store nothing), so every broadcast operand read from the tiles serves two
+// rows — half the shared-memory wavefronts per inverse of the one-row-per-lane
+// half-warp version, and four blocks per warp instead of two. The arithmetic
+// of every row is hw_spd_inverse_v2's (same operations in the same order), so
+// the results are bitwise equal to it.
+// a0, a1: rows l, l + H of W (consumed). Lr: [N][N] rows of L — may be the
+// source block itself (in place: the routine first waits until every lane
+// holds its rows). LiT: [N][N] rows of L^-T (may alias Lr). rd: [N].
+// x0, x1: rows l, l + H of W^-1 (bitwise symmetric: also its columns).
+// Every lane of the warp must call it (full-warp syncs, width-8 shuffles).
+// Returns the first failing pivot (group-uniform) or -1.
+template <class T, int N>
+__device__ __forceinline__ int g8x2_spd_inverse(T (&a0)[N], T (&a1)[N], T* Lr, T* LiT, T* rd, int l,
+                                                T (&x0)[N], T (&x1)[N]) {
+  static_assert(N % 2 == 0 && N <= 16, "even N <= 16");
+  constexpr int H = N / 2;
+  const bool act = l < H;
+  const int lr = act ? l : H - 1;
+  int fail = -1;
+  __syncwarp();  // Lr may be the source block: every lane has read its rows
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    T s0 = T(0), s1 = a1[k];
+    if (k < H) s0 = a0[k];
+#pragma unroll
+    for (int q = 0; q < k; ++q) {
+      const T v = Lr[k * N + q];
+      if (k < H) s0 -= a0[q] * v;
+      s1 -= a1[q] * v;
+    }
+    T piv = __shfl_sync(FULL, k < H ? s0 : s1, k < H ? k : k - H, 8);
+    const bool bad = piv <= T(0);  // x <= 0 fails, NaN passes (Eigen LLT)
+    fail = (bad && fail < 0) ? k : fail;
+    piv = bad ? T(1) : piv;
+    const T r = rsqrt(piv);
+    if (k < H) {
+      const T v0 = (lr == k ? piv : s0) * r;
+      const bool own0 = act && lr >= k;
+      a0[k] = own0 ? v0 : a0[k];
+      if (own0) Lr[lr * N + k] = v0;
+    }
+    {
+      const T v1 = (lr + H == k ? piv : s1) * r;
+      const bool own1 = act && lr + H >= k;
+      a1[k] = own1 ? v1 : a1[k];
+      if (own1) Lr[(lr + H) * N + k] = v1;
+    }
+    if (act && lr == (k < H ? k : k - H)) rd[k] = r;
+    __syncwarp();
+  }
+  // columns l and l + H of L^-1
+  T y0[N], y1[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T t0 = (i == lr) ? T(1) : T(0), t1 = (i == lr + H) ? T(1) : T(0);
+#pragma unroll
+    for (int q = 0; q < i; ++q) {
+      const T v = Lr[i * N + q];
+      t0 -= v * y0[q];
+      t1 -= v * y1[q];
+    }
+    const T d = rd[i];
+    y0[i] = t0 * d;
+    y1[i] = t1 * d;
+  }
+  __syncwarp();  // LiT may alias Lr
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < N; q += 2) {
+      *reinterpret_cast<double2*>(LiT + lr * N + q) = make_double2(y0[q], y0[q + 1]);
+      *reinterpret_cast<double2*>(LiT + (lr + H) * N + q) = make_double2(y1[q], y1[q + 1]);
+    }
+  }
+  __syncwarp();
+  // X[i][c] = sum_{q >= i} LiT[i][q] y_c[q]; y_c[i] dies with row i
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    T s0 = T(0), s1 = T(0);
+#pragma unroll
+    for (int q = i; q < N; ++q) {
+      const T v = LiT[i * N + q];
+      s0 += v * y0[q];
+      s1 += v * y1[q];
+    }
+    x0[i] = s0;
+    x1[i] = s1;
+  }
+  __syncwarp();
+  return fail;
+}
+
 // hw_spd_inverse_v2 for N <= 8 on 8-lane groups: a half-warp inverts two
 // independent matrices at once (lanes 0-7 and 8-15). l = lane & 7; every lane
 // of the warp must call it (full-warp mask, width-8 shuffles); Lr / LiT / rd

@@ -43,12 +43,12 @@ cyc = np.stack([seg[:, 0] & 0xffffffff, seg[:, 0] >> 32, seg[:, 1] & 0xffffffff,
 segn = ["Srows", "ups_reduce", "update_precond", "eta_reduce", "beta_p_barrier"]
 print(json.dumps({"pcg_cycles_per_iter": {nm: round(float(np.mean(cyc[:, i] / its)), 1)
                                           for i, nm in enumerate(segn)}}))
-if KN > 32:
-    print(json.dumps({"F1_split_us": {
-        "q_wait": float(np.mean(steady[:, 11] - steady[:, 0]) / 1e3),
-        "Q_round0": float(np.mean(steady[:, 8] - steady[:, 11]) / 1e3),
-        "Q_round1": float(np.mean(steady[:, 9] - steady[:, 8]) / 1e3),
-        "R_inv": float(np.mean(steady[:, 10] - steady[:, 9]) / 1e3),
-        "barrier": float(np.mean(steady[:, 1] - steady[:, 10]) / 1e3)}}))
+print(json.dumps({"F1_split_us": {
+    "q_wait": float(np.mean(steady[:, 11] - steady[:, 0]) / 1e3),
+    "Q_inv": float(np.mean(steady[:, 8] - steady[:, 11]) / 1e3),
+    "R_inv": float(np.mean(steady[:, 9] - steady[:, 8]) / 1e3),
+    "barrier": float(np.mean(steady[:, 1] - steady[:, 9]) / 1e3)}}))
+print(json.dumps({"F2_split_us": {"products": float(np.mean(steady[:, 10] - steady[:, 1]) / 1e3),
+                                  "theta_inv": float(np.mean(steady[:, 2] - steady[:, 10]) / 1e3)}}))
 first = np.diff(b[:G, :5], axis=1) / 1e3
 print(json.dumps({"first_wave_us": {nm: float(np.mean(first[:, i])) for i, nm in enumerate(names)}}))
