@@ -47,12 +47,21 @@ struct FLayout {
   // 8-lane group tiles of F1 (L^-T of Q_g, then the R_g^-1 tiles) and of the
   // theta^-1 pass: [max(n n, 2 MB MB)] | rd [16]
   static constexpr int g8_tile = (NB * NB > 2 * MB * MB ? NB * NB : 2 * MB * MB) + 16;
-  static constexpr int tiles = kHalfWarps * per_hw > 64 * g8_tile ? kHalfWarps * per_hw : 64 * g8_tile;
+  static constexpr int tiles0 = kHalfWarps * per_hw > 64 * g8_tile ? kHalfWarps * per_hw : 64 * g8_tile;
   __host__ __device__ static int oQi(int) { return 0; }
   __host__ __device__ static int oqq(int K) { return K * NB * NB; }
   __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
   __host__ __device__ static int ohw(int K) { return orr(K) + (K - 1) * 8; }
-  __host__ __device__ static int osq(int K) { return ohw(K) + tiles; }  // q_k
+  // The tile region also holds, at its end, the D blocks F2 leaves in place for
+  // the PCG (theta_1..theta_63, D_0 = Q_0^-1 before them: oD); it is sized so
+  // they clear the PCG's staged L (padded stride) and vectors below them.
+  __host__ __device__ static int tiles(int K) {
+    const int ls = NB * NB + ((8 - (NB * NB) % 32) + 32) % 32;  // fused_ls(NB)
+    const int need = K * ls + 3 * K * NB + 32 - ohw(K) + 64 * NB * NB;
+    return tiles0 > need ? tiles0 : need;
+  }
+  __host__ __device__ static int oD(int K) { return ohw(K) + tiles(K) - 64 * NB * NB; }
+  __host__ __device__ static int osq(int K) { return ohw(K) + tiles(K); }  // q_k
   __host__ __device__ static int total(int K) { return osq(K) + K * NB; }
 };
 
@@ -115,6 +124,14 @@ __device__ __forceinline__ void mbar_wait(unsigned mbar_addr, unsigned& phase) {
   phase ^= 1u;
 }
 
+// D = A B + D on the FP64 tensor cores (m8n8k4, A row-major, B column-major
+// fragments): bitwise the FMA chain d = fma(a_k, b_k, d) over k = 0..3.
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
 // ---- Tensor memory (TMEM) as a third on-chip operand store for the PCG
 // phase: 512 columns x 128 lanes x 32 bit; thread t of warp w owns TMEM lane
 // 32*(w%4) + t%32 and columns [128*(w/4), 128*(w/4) + 128): rows pi and
@@ -166,11 +183,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   // region past `red`); sL: the L blocks at the padded stride LS.
   constexpr int LS = fused_ls(NB);
   T* sL = smem;                                 // [K][LS]  staging only
-  T* sD = smem + static_cast<size_t>(K) * LS;   // [K][NB][NB]  D row products
-  T* sp = sD + static_cast<size_t>(K) * NN;     // [K][NB]
+  T* sp = smem + static_cast<size_t>(K) * LS;   // [K][NB]
   T* st = sp + K * NB;
   T* su = st + K * NB;
-  T* red = su + K * NB;                  // [64]
+  T* red = su + K * NB;                         // [32]
+  // D_b rows stay where the formation left them: theta_b (b >= 1) at the end
+  // of the tile region (F2), D_0 = Q_0^-1 just before (FLayout::oD)
+  T* sD = smem + FL::oD(K);                     // [K][NB][NB]  D row products
   // formation layout (aliases the PCG layout; phases are separated by barriers)
   T* sQi = smem + FL::oQi(K);   // [K][NB][NB], column l written by lane l
   T* sqq = smem + FL::oqq(K);   // [K][16]  Q_k^-1 q_k
@@ -351,196 +370,280 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 
     if (tm) tm[1] = gtimer();
     // ============================================================ F2: rows
+    // schur.cpp:58-78 on the FP64 tensor cores. Warp w forms rows b = w + 16 t
+    // (one row at a time, warp-uniform): every block product is a chain of
+    // mma.sync.m8n8k4.f64 over 16 x 16 tiles (n padded with zeros), k-steps in
+    // ascending order. DMMA D = A B + C equals the scalar FMA chain from C over
+    // k = 0..3 bitwise (scripts/micro/dmma_round.cu), so each element is the
+    // same fma chain, in the same order, as the scalar row products — and as
+    // the reference's dot products in order — with zero pads adding exact zeros.
+    //   AQ = A_k Q_k^-1 (pad column NB of Q_k^-1 carries Q_k^-1 q_k, so column
+    //   NB of AQ is A (Q^-1 q) for zeta), L_b = -AQ;
+    //   BR = B_k R_k^-1 (pad column MB carries R_k^-1 r_k: B (R^-1 r));
+    //   theta_raw = (AQ A' + BR B') + Q_{k+1}^-1, theta = (theta_raw + theta_raw')/2;
+    //   gamma_b = e_k - zeta.
+    // The warp's tile (stride 20: the A-fragment reads are conflict-free) moves
+    // accumulator fragments into A-operand fragments and transposes theta_raw.
+    {
+      constexpr bool PADQ = NB < 16, PADR = MB < 8;
+      const int w = tid >> 5, fr = lane >> 2, fc = lane & 3;
 #pragma unroll 1
-    for (int r = 0; r < R; ++r) {
-      const int b0 = h + r * kHalfWarps;
-      // rows outside [1, K) run the general path on row 1 and store nothing
-      // (keeps the two half-warps convergent for the full-warp shuffles)
-      const bool wr = b0 >= 1 && b0 < K;
-      const int b = wr ? b0 : 1;
-      if (b0 == 0) {
-        // schur.cpp:53-57: S(0,0) = Q0^-1, theta_inv[0] = sym(Q0), gamma_0
-        if (lact) {
-          gG[l] = -((xs[l] - x0[l]) + sqq[l]);
-          if (p.form_only) {
-            T* So = p.S_out + static_cast<size_t>(sys) * K * 3 * nn;
+      for (int t = 0; t < 4; ++t) {
+        const int b = w + 16 * t;
+        const bool live = b >= 1 && b < K;  // warp-uniform
+        if (b == 0) {
+          // schur.cpp:53-57: S(0,0) = D_0 = Q_0^-1, theta_inv[0] = sym(Q_0), gamma_0
+          if (lane < NB) {
+            const T g0 = -((xs[lane] - x0[lane]) + sqq[lane]);
+            gG[lane] = g0;
+            if (p.form_only) p.gamma_out[static_cast<size_t>(sys) * K * NB + lane] = g0;
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-              So[nn + i * NB + l] = sQi[i * NB + l];
-              p.theta_out[static_cast<size_t>(sys) * K * nn + i * NB + l] =
-                  T(0.5) * (Qs[l * NB + i] + Qs[i * NB + l]);
+            for (int j = 0; j < NB; ++j) {
+              const T d = sQi[lane * NB + j];
+              smem[FL::oD(K) + lane * NB + j] = d;  // D_0 in place for the PCG
+              if (p.form_only) {
+                p.S_out[static_cast<size_t>(sys) * K * 3 * nn + nn + lane * NB + j] = d;
+                p.theta_out[static_cast<size_t>(sys) * K * nn + lane * NB + j] =
+                    T(0.5) * (Qs[lane * NB + j] + Qs[j * NB + lane]);
+              }
             }
-            p.gamma_out[static_cast<size_t>(sys) * K * NB + l] = gG[l];
           }
         }
-      }
-      const int k = b - 1;
-      const T* Ak = As + k * nn;
-      const T* Bk = Bs + k * nm;
-      T x[NB];
-      // A_k -> the tX tile with asynchronous 16-byte copies (one L2 round trip,
-      // no registers held), then AQ = A_k Q_k^-1 column l from shared memory
-      // -> L_b = phi = -AQ (schur.cpp:68)
-      // R_k^-1 (from the slot, 8-byte aligned) -> the tW tile the same way
-      T brow[MB];
+        if (live) {
+          const int k = b - 1;
+          const T* Ak = As + static_cast<size_t>(k) * nn;
+          const T* Bk = Bs + static_cast<size_t>(k) * nm;
+          const T* Xk = sQi + static_cast<size_t>(k) * NN;
+          const T* Xk1 = Xk + NN;
+          // operand fragments: A (row r, col c), B (row c, col r)
+          T af[2][4], bf[2][2], xf[2][4], rf[2];
 #pragma unroll
-      for (int q = 0; q < MB; ++q) brow[q] = (EXM || q < m) ? __ldg(Bk + lr * m + q) : T(0);
-      {
-        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(tX));
-        for (int c = l; c < NN / 2; c += 16)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16u * c),
-                       "l"(Ak + 2 * c)
-                       : "memory");
-        const unsigned dr = static_cast<unsigned>(__cvta_generic_to_shared(tW));
-        for (int c = l; c < MB * MB; c += 16)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dr + 8u * c),
-                       "l"(gR + static_cast<size_t>(k) * mm + c)
-                       : "memory");
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-      }
-      __syncwarp();
-      // BR = B_k R_k^-1, row l (R_k^-1 rows are broadcasts)
-      T br[MB];
+          for (int mt = 0; mt < 2; ++mt) {
+            const int i = mt * 8 + fr;
 #pragma unroll
-      for (int q = 0; q < MB; ++q) br[q] = T(0);
+            for (int ks = 0; ks < 4; ++ks) {
+              const int q = ks * 4 + fc;
+              af[mt][ks] = (i < NB && q < NB) ? __ldg(Ak + i * NB + q) : T(0);
+            }
 #pragma unroll
-      for (int s2 = 0; s2 < MB; ++s2) {
-#pragma unroll
-        for (int q = 0; q < MB; ++q) br[q] += brow[s2] * tW[s2 * MB + q];
-      }
-      T qc[NB];
-#pragma unroll
-      for (int q = 0; q < NB; ++q) qc[q] = sQi[k * NN + q * NB + lr];
-      __syncwarp();
-      {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          T s = T(0);
-#pragma unroll
-          for (int q = 0; q < NB; q += 2) {
-            const double2 a2 = *reinterpret_cast<const double2*>(tX + i * NB + q);
-            s += a2.x * qc[q];
-            s += a2.y * qc[q + 1];
+            for (int ks = 0; ks < 2; ++ks) {
+              const int q = ks * 4 + fc;
+              bf[mt][ks] = (i < NB && q < m && (EXM || q < MB)) ? __ldg(Bk + i * m + q) : T(0);
+            }
           }
-          x[i] = s;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int j = nt * 8 + fr;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const int q = ks * 4 + fc;
+              T v = T(0);
+              if (q < NB) v = j < NB ? Xk[q * NB + j] : ((PADQ && j == NB) ? sqq[k * 16 + q] : T(0));
+              xf[nt][ks] = v;
+            }
+          }
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int sr = ks * 4 + fc;
+            T v = T(0);
+            if (sr < MB)
+              v = fr < MB ? __ldcg(gR + static_cast<size_t>(k) * mm + sr * MB + fr)
+                          : ((PADR && fr == MB) ? srr[k * 8 + sr] : T(0));
+            rf[ks] = v;
+          }
+          // AQ (16 DMMA)
+          T aq[2][2][2];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              aq[mt][nt][0] = aq[mt][nt][1] = T(0);
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) dmma_f64(aq[mt][nt][0], aq[mt][nt][1], af[mt][ks], xf[nt][ks]);
+            }
+          // BR (4 DMMA), cols 0..7
+          T br[2][2];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            br[mt][0] = br[mt][1] = T(0);
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) dmma_f64(br[mt][0], br[mt][1], bf[mt][ks], rf[ks]);
+          }
+          // L_b = -AQ -> slot (padded stride LS) and, for build_schur, S.left(b) / S.right(b-1)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const int i = mt * 8 + fr, j = nt * 8 + 2 * fc;
+              if (i < NB && j < NB) {
+                *reinterpret_cast<double2*>(gL + static_cast<size_t>(b) * LS + i * NB + j) =
+                    make_double2(-aq[mt][nt][0], -aq[mt][nt][1]);
+                if (p.form_only) {
+                  T* Sl = p.S_out + (static_cast<size_t>(sys) * K + b) * 3 * nn;
+                  T* Sr = p.S_out + ((static_cast<size_t>(sys) * K + b - 1) * 3 + 2) * nn;
+                  Sl[i * NB + j] = -aq[mt][nt][0];
+                  Sl[i * NB + j + 1] = -aq[mt][nt][1];
+                  Sr[j * NB + i] = -aq[mt][nt][0];
+                  Sr[(j + 1) * NB + i] = -aq[mt][nt][1];
+                }
+              }
+            }
+          // zeta_i = (-A(Q^-1 q) - B(R^-1 r)) + Q_{k+1}^-1 q_{k+1}; gamma_b = e_k - zeta
+          // (the pad columns NB of AQ and MB of BR sit in lanes (r, NB%8/2) and
+          // (r, MB/2); lane (r, 0) gathers them)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const int i = mt * 8 + fr;
+            T aqq = T(0), brr = T(0);
+            if constexpr (PADQ) aqq = __shfl_sync(FULL, aq[mt][NB / 8][(NB % 8) & 1], fr * 4 + (NB % 8) / 2);
+            if constexpr (PADR) brr = __shfl_sync(FULL, br[mt][MB & 1], fr * 4 + MB / 2);
+            if (fc == 0 && i < NB) {
+              if constexpr (!PADQ) {
+#pragma unroll
+                for (int q = 0; q < NB; ++q) aqq += __ldg(Ak + i * NB + q) * sqq[k * 16 + q];
+              }
+              if constexpr (!PADR) {
+#pragma unroll
+                for (int q = 0; q < MB; ++q)
+                  brr += ((EXM || q < m) ? __ldg(Bk + i * m + q) : T(0)) * srr[k * 8 + q];
+              }
+              const T zeta = (-aqq - brr) + sqq[(k + 1) * 16 + i];
+              const T g = -(-__ldg(es + k * NB + i) + zeta);
+              gG[static_cast<size_t>(b) * NB + i] = g;
+              if (p.form_only) p.gamma_out[(static_cast<size_t>(sys) * K + b) * NB + i] = g;
+            }
+          }
+          // accumulator fragment (row r, cols 2c, 2c+1 of a tile) -> A-operand
+          // fragment (row r, col c of a k-step): quad shuffles
+          auto to_a = [&](const T (&d)[2], int col) {  // col: column inside the 8-wide tile
+            const int src = fr * 4 + (col >> 1);
+            const T v0 = __shfl_sync(FULL, d[0], src), v1 = __shfl_sync(FULL, d[1], src);
+            return (col & 1) ? v1 : v0;
+          };
+          // AQ as A operand (pad columns zeroed: no leak of the zeta column)
+          T aqa[2][4];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const T v = to_a(aq[mt][ks >> 1], (ks & 1) * 4 + fc);
+              aqa[mt][ks] = ks * 4 + fc < NB ? v : T(0);
+            }
+          // theta_A = AQ A' (16 DMMA): B operand (row q, col j) = A[j][q] = af
+          T ta[2][2][2];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              ta[mt][nt][0] = ta[mt][nt][1] = T(0);
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) dmma_f64(ta[mt][nt][0], ta[mt][nt][1], aqa[mt][ks], af[nt][ks]);
+            }
+          T bra[2][2];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const T v = to_a(br[mt], ks * 4 + fc);
+              bra[mt][ks] = ks * 4 + fc < MB ? v : T(0);
+            }
+          // theta_raw = (AQ A' + BR B') + Q_{k+1}^-1 (schur.cpp:65-66)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              T s0 = T(0), s1 = T(0);
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) dmma_f64(s0, s1, bra[mt][ks], bf[nt][ks]);
+              const int i = mt * 8 + fr, j = nt * 8 + 2 * fc;
+              double2 x1 = make_double2(0.0, 0.0);
+              if (i < NB && j < NB) x1 = *reinterpret_cast<const double2*>(Xk1 + i * NB + j);
+              ta[mt][nt][0] = (ta[mt][nt][0] + s0) + x1.x;
+              ta[mt][nt][1] = (ta[mt][nt][1] + s1) + x1.y;
+            }
+          // theta = (theta_raw + theta_raw')/2 (schur.cpp:67): the transposed
+          // element (j, i) of lane (r, c)'s (i, j) = (8 mt + r, 8 nt + 2c + e)
+          // sits in lane (2c + e, r / 2), tile (nt, mt), element r & 1
+          T* thb = smem + FL::oD(K) + static_cast<size_t>(b) * NN;  // = the PCG's D_b
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              const int i = mt * 8 + fr, j = nt * 8 + 2 * fc;
+              T tr[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int src = (2 * fc + e) * 4 + (fr >> 1);
+                const T v0 = __shfl_sync(FULL, ta[nt][mt][0], src), v1 = __shfl_sync(FULL, ta[nt][mt][1], src);
+                tr[e] = (fr & 1) ? v1 : v0;
+              }
+              const T t0 = T(0.5) * (ta[mt][nt][0] + tr[0]);
+              const T t1 = T(0.5) * (ta[mt][nt][1] + tr[1]);
+              if (i < NB && j < NB) {
+                // theta_b rows for the theta^-1 pass (shared memory)
+                *reinterpret_cast<double2*>(thb + i * NB + j) = make_double2(t0, t1);
+                if (p.form_only) {
+                  T* Sd = p.S_out + ((static_cast<size_t>(sys) * K + b) * 3 + 1) * nn;
+                  Sd[i * NB + j] = t0;
+                  Sd[i * NB + j + 1] = t1;
+                }
+              }
+            }
+          __syncwarp();
         }
-      }
-      T arow[NB];
-#pragma unroll
-      for (int q = 0; q < NB; q += 2) {
-        const double2 a2 = *reinterpret_cast<const double2*>(tX + lr * NB + q);
-        arow[q] = a2.x;
-        arow[q + 1] = a2.y;
-      }
-      __syncwarp();  // A_k and R_k^-1 tiles consumed
-      if (lact) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          tW[i * LD + l] = x[i];
-          if (wr) gL[static_cast<size_t>(b) * LS + i * NB + l] = -x[i];
-          if (wr && p.form_only)  // S.left(b) = phi (schur.cpp:74)
-            p.S_out[(static_cast<size_t>(sys) * K + b) * 3 * nn + i * NB + l] = -x[i];
-        }
-#pragma unroll
-        for (int q = 0; q < MB; ++q) tBR[l * LDM + q] = br[q];
-      }
-      __syncwarp();
-      if (wr && lact && p.form_only) {  // S.right(b-1) = phi' (schur.cpp:74)
-#pragma unroll
-        for (int j = 0; j < NB; ++j)
-          p.S_out[((static_cast<size_t>(sys) * K + b - 1) * 3 + 2) * nn + j * NB + l] =
-              -tW[lr * LD + j];
-      }
-      // theta_raw column l = (AQ A')(:,l) + (BR B')(:,l) + Q_{k+1}^-1(:,l)  (schur.cpp:65-66)
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        T s1 = T(0), s2 = T(0);
-#pragma unroll
-        for (int q = 0; q < NB; ++q) s1 += tW[i * LD + q] * arow[q];
-#pragma unroll
-        for (int q = 0; q < MB; ++q) s2 += tBR[i * LDM + q] * brow[q];
-        x[i] = (s1 + s2) + sQi[(k + 1) * NN + i * NB + lr];
-      }
-      // zeta = -A (Q_k^-1 q_k) - B (R_k^-1 r_k) + Q_{k+1}^-1 q_{k+1}; gamma (schur.cpp:69-77)
-      {
-        T aqq = T(0), brr = T(0);
-#pragma unroll
-        for (int q = 0; q < NB; ++q) aqq += arow[q] * sqq[k * 16 + q];
-#pragma unroll
-        for (int q = 0; q < MB; ++q) brr += brow[q] * srr[k * 8 + q];
-        const T zeta = (-aqq - brr) + sqq[(k + 1) * 16 + lr];
-        if (wr && lact) {
-          const T g = -(-__ldg(es + k * NB + l) + zeta);
-          gG[static_cast<size_t>(b) * NB + l] = g;
-          if (p.form_only) p.gamma_out[(static_cast<size_t>(sys) * K + b) * NB + l] = g;
-        }
-      }
-      hw_symmetrize_col<T, NB, LD, true>(tW, l, x);  // theta (schur.cpp:67)
-      if ((wr || b0 == 0) && lact) {
-        // D_b = theta (row 0: Q_0^-1, schur.cpp:53) -> the slot, stored as columns
-        // (both are bitwise symmetric, so column l = row l): the PCG phase stages
-        // it into TMEM in its own row mapping
-        const int bd = b0 == 0 ? 0 : b;
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
-          const T d = (b0 == 0) ? sQi[lr * NB + i] : x[i];
-          gD[static_cast<size_t>(bd) * nn + i * NB + l] = d;
-          if (p.form_only)  // S.diag(b) = theta (schur.cpp:73)
-            p.S_out[((static_cast<size_t>(sys) * K + bd) * 3 + 1) * nn + i * NB + l] = d;
-        }
-      }
-      // theta_b -> knot b-1's Q^-1 region for the theta^-1 pass: dead once every
-      // half-warp has finished this round (round 0: knots 0..30, round 1: 31..62)
-      __syncthreads();
-      if (wr && lact) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) sQi[(b - 1) * NN + i * NB + l] = x[i];
       }
     }
     // ===================================================== theta^-1 (schur.cpp:75)
     // One pass over all rows on 8-lane groups: group b = tid / 8, lane gl owns
     // rows gl and gl + n/2 — exactly the PCG's quarter-warp mapping, so the
     // inverse's output rows ARE the PCG thread's theta_b^-1 register rows
-    // (no slot round trip). theta_b is read from shared memory (F2 left it in
-    // knot b-1's region).
-    T ti[2][NB];
-    __syncthreads();  // every theta_b is in place; the formation tiles are free
+    // (no slot round trip). theta_b is read from the lower triangle F2 left in
+    // shared memory.
+    __syncthreads();  // every theta_b is in place
     if (tm) tm[10] = gtimer();
-    {
+    // warps wholly past the horizon skip the pass (their PCG rows are discarded)
+    if (4 * (tid >> 5) < K) {
       constexpr int H = NB / 2;
       const int b = tid >> 3, gl = tid & 7;
       const int glr = gl < H ? gl : H - 1;
-      // row 0 and rows past the horizon invert a clamped theta (row 1 / K-1)
-      // in their own tile and keep nothing: convergent full-warp syncs
+      // row 0 and the horizon warp's rows past K invert a clamped theta (row
+      // 1 / K-1) in their own tile and keep nothing: convergent full-warp syncs
+      // (their tiles, b < K + 3, stay clear of the theta triangles)
       const int bi = b == 0 ? 1 : (b < K ? b : K - 1);
-      T* gt = smem + FL::ohw(K) + static_cast<size_t>(b) * FL::g8_tile;
+      T* gt = smem + static_cast<size_t>(b) * FL::g8_tile;  // sQi region (dead)
       T a0[NB], a1[NB];
-      const T* Th = sQi + static_cast<size_t>(bi - 1) * nn + glr * NB;
+      const T* Th = smem + FL::oD(K) + static_cast<size_t>(bi) * NN + glr * NB;
 #pragma unroll
       for (int i = 0; i < NB; i += 2) {
         const double2 u = *reinterpret_cast<const double2*>(Th + i);
         const double2 v = *reinterpret_cast<const double2*>(Th + H * NB + i);
         a0[i] = u.x; a0[i + 1] = u.y; a1[i] = v.x; a1[i + 1] = v.y;
       }
-      const int f = g8x2_spd_inverse<T, NB>(a0, a1, gt, gt, gt + FL::g8_tile - 16, gl, ti[0], ti[1]);
+      T x0[NB], x1[NB];
+      if (tm) tm[13] = gtimer();
+      const int f = g8x2_spd_inverse<T, NB>(a0, a1, gt, gt, gt + FL::g8_tile - 16, gl, x0, x1);
+      if (tm) tm[14] = gtimer();
       if (b >= 1 && b < K && f >= 0) fkey = min(fkey, b * 4 + 3);
-      if (b == 0) {  // theta_inv[0] = sym(Q_0), not an inverse (schur.cpp:55)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int row = glr + H * c;
-#pragma unroll
-          for (int j = 0; j < NB; ++j) ti[c][j] = T(0.5) * (Qs[row * NB + j] + Qs[j * NB + row]);
-        }
-      }
+      // (row 0's theta_inv[0] = sym(Q_0) is read by the PCG stage itself)
       if (p.form_only && b >= 1 && b < K && gl < H) {  // theta_inv[b] rows
         T* To = p.theta_out + (static_cast<size_t>(sys) * K + b) * nn;
 #pragma unroll
         for (int j = 0; j < NB; ++j) {
-          To[glr * NB + j] = ti[0][j];
-          To[(glr + H) * NB + j] = ti[1][j];
+          To[glr * NB + j] = x0[j];
+          To[(glr + H) * NB + j] = x1[j];
+        }
+      }
+      // the rows stay in the group's (now free) tile until the PCG stage loads
+      // them into the same thread's registers
+      if (gl < H) {
+#pragma unroll
+        for (int j = 0; j < NB; j += 2) {
+          *reinterpret_cast<double2*>(gt + glr * NB + j) = make_double2(x0[j], x0[j + 1]);
+          *reinterpret_cast<double2*>(gt + (glr + H) * NB + j) = make_double2(x1[j], x1[j + 1]);
         }
       }
     }
+    if (tm) tm[12] = gtimer();
     // F2's global writes (L, D, gamma) are read back by the async proxy (TMA)
     // below: order them before the barrier
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -577,18 +680,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     const int pbl = pbc > 0 ? pbc - 1 : 0;          // neighbours, clamped into [0, K):
     const int pbn = pbc + 1 < K ? pbc + 1 : K - 1;  // edge products are discarded
     const int pr = pi < H ? pi : H - 1;             // clamped row (idle lanes)
+    // theta_b^-1 rows pr, pr + n/2: the thread's own group tile (theta^-1 pass),
+    // read before the staging copies overwrite the tiles
+    T ti[2][NB];
     {
-      // stage D and L from the slot (one TMA bulk copy each), then every thread
-      // moves its own rows into its TMEM lane
-      const unsigned bd = static_cast<unsigned>(sizeof(T) * K * NN);
+      const T* tt = smem + static_cast<size_t>(pb) * FL::g8_tile + pr * NB;
+#pragma unroll
+      for (int j = 0; j < NB; j += 2) {
+        const double2 u = 4 * (tid >> 5) < K ? *reinterpret_cast<const double2*>(tt + j) : make_double2(0.0, 0.0);
+        const double2 v = 4 * (tid >> 5) < K ? *reinterpret_cast<const double2*>(tt + H * NB + j) : make_double2(0.0, 0.0);
+        ti[0][j] = u.x; ti[0][j + 1] = u.y; ti[1][j] = v.x; ti[1][j + 1] = v.y;
+      }
+    }
+    __syncthreads();
+    {
+      // stage L from the slot (one TMA bulk copy), then every thread moves its
+      // L_b rows and R_b = L_{b+1}' rows into its TMEM lane
       const unsigned bl = static_cast<unsigned>(sizeof(T) * K * LS);
       if (tid == 0) {
         asm volatile("fence.proxy.async;\n" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar_addr),
-                     "r"(bd + bl)
+                     "r"(bl)
                      : "memory");
-        tma_copy_1d(sD, gD, bd, mbar_addr);
         tma_copy_1d(sL, gL, bl, mbar_addr);
+      }
+    }
+    if (pb == 0) {  // theta_inv[0] = sym(Q_0), not an inverse (schur.cpp:55)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int row = pr + H * c;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) ti[c][j] = T(0.5) * (__ldg(Qs + row * NB + j) + __ldg(Qs + j * NB + row));
       }
     }
     T lam[2], rr[2], rt[2], pp[2], spv[2], best[2], gam[2];
@@ -787,7 +909,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int c = 0; c < 2; ++c)
           if (pact) up += pp[c] * spv[c];
         segmark(0);
-        const T ups = block_reduce(up, red + 32);  // buffer B
+        const T ups = block_reduce(up, red + 16);  // buffer B
         segmark(1);
         if (!is_finite(ups)) {
           code = kRuntime;
@@ -964,7 +1086,13 @@ bool fused_supported(int K, int n, int m, int kind) {
   if (kind == kPoly) return false;
   if (K < 2 || K > 2 * kHalfWarps) return false;
   return with_fused_shape(n, m, [&](auto nb, auto mb, auto) {
-    return fused_smem_bytes<T, decltype(nb)::value, decltype(mb)::value>(K) + 64 <= 227 * 1024;
+    constexpr int NB = decltype(nb)::value, MB = decltype(mb)::value;
+    using FL = FLayout<T, NB, MB>;
+    // the theta^-1 pass's group tiles (groups < K + 3) stay clear of the theta
+    // rows F2 leaves at the end of the tile region
+    // (and of the D blocks left in place, oD)
+    const bool tiles_ok = (K + 3) * FL::g8_tile <= FL::oD(K);
+    return tiles_ok && fused_smem_bytes<T, NB, MB>(K) + 64 <= 227 * 1024;
   });
 }
 

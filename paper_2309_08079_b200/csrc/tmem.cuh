@@ -6,6 +6,12 @@
 namespace b2p {
 namespace tm {
 
+// doubles per TMEM load chunk in the row products (2 rows x 2 words each live
+// in registers between the load and its wait)
+#ifndef TM_CHUNK
+#define TM_CHUNK 4
+#endif
+
 __device__ __forceinline__ void ld16(unsigned t, unsigned* u) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
@@ -123,7 +129,7 @@ template <int NB, int J0>
 __device__ __forceinline__ void dot2_chunks(unsigned t0, unsigned t1, const double* x, double& a0,
                                             double& c0, double& a1, double& c1) {
   if constexpr (J0 < NB) {
-    constexpr int C = (NB - J0) < 8 ? (NB - J0) : 8;  // doubles in this chunk (even)
+    constexpr int C = (NB - J0) < TM_CHUNK ? (NB - J0) : TM_CHUNK;  // doubles in this chunk (even)
     unsigned u[2 * C], w[2 * C];
     ld_words<2 * C>(t0 + 2 * J0, u);
     ld_words<2 * C>(t1 + 2 * J0, w);

@@ -49,6 +49,9 @@ print(json.dumps({"F1_split_us": {
     "R_inv": float(np.mean(steady[:, 9] - steady[:, 8]) / 1e3),
     "barrier": float(np.mean(steady[:, 1] - steady[:, 9]) / 1e3)}}))
 print(json.dumps({"F2_split_us": {"products": float(np.mean(steady[:, 10] - steady[:, 1]) / 1e3),
-                                  "theta_inv": float(np.mean(steady[:, 2] - steady[:, 10]) / 1e3)}}))
+                                  "theta_inv": float(np.mean(steady[:, 12] - steady[:, 10]) / 1e3),
+                                  "theta_inv_load": float(np.mean(steady[:, 13] - steady[:, 10]) / 1e3),
+                                  "theta_inv_routine": float(np.mean(steady[:, 14] - steady[:, 13]) / 1e3),
+                                  "fence": float(np.mean(steady[:, 2] - steady[:, 12]) / 1e3)}}))
 first = np.diff(b[:G, :5], axis=1) / 1e3
 print(json.dumps({"first_wave_us": {nm: float(np.mean(first[:, i])) for i, nm in enumerate(names)}}))
