@@ -348,11 +348,38 @@ def c1_graph_latency(api, torch, local, reps=200, N=31, n=14, m=7):
             "matches_eager": ok}
 
 
-def nmpc_batch_throughput(api, torch, local, B=4096, N=32, n=2, m=1, reps=5):
+def shape_batch(api, torch, local, B, N, n, m, reps=5, check=64, c4_tflops=None):
+    """An off-BASELINE shape as a device-resident batch (the reference forms and
+    solves any (n, m), schur.cpp:38-82): solves/s, the kernel that ran,
+    reference-algorithm flop throughput beside the c4 one (SURVEY 8d F_full with
+    the measured iterations), and per-system parity against the oracle on the
+    first `check` systems (outside the timed region)."""
+    r = nmpc_batch_throughput(api, torch, local, B=B, N=N, n=n, m=m, reps=reps, seed=4242,
+                              keep=True)
+    lam, reports, kb = r.pop("_lam"), r.pop("_reports"), r.pop("_kkt")
+    alg = algorithmic(N, n, m, r["iters_mean"])
+    r["tflops_ref_algorithm"] = B * alg["f_full"] / (r["ms_per_batch"] * 1e-3) / 1e12
+    if c4_tflops:
+        r["per_flop_vs_c4"] = r["tflops_ref_algorithm"] / c4_tflops
+    orc = _orc()
+    sub = orc.random_kkt_batch(4242, check, N, n, m)
+    _, lo, ro = orc.solve_batch(sub, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
+    it_gpu = np.asarray(reports.iterations[:check])
+    it_orc = np.array([x.iterations for x in ro])
+    lg = lam[:check]
+    scale = np.maximum(1.0, np.abs(lo).max(axis=1))
+    r["parity"] = {"systems": check, "iterations_equal": int((it_gpu == it_orc).sum()),
+                   "lambda_rel_err_max": float((np.abs(lg - lo).max(axis=1) / scale).max()),
+                   "tolerance": 1e-10}
+    return r
+
+
+def nmpc_batch_throughput(api, torch, local, B=4096, N=32, n=2, m=1, reps=5, seed=77,
+                          keep=False):
     """Many independent NMPC-shape systems (double-integrator / pendulum size, the
     SQP callers' shape) through the small-block kernel, device-resident, CUDA events."""
     from paper_2309_08079_b200.types import KKTSystem
-    kb = api.random_kkt_batch(77, B, N, n, m)
+    kb = api.random_kkt_batch(seed, B, N, n, m)
     dev = [torch.from_numpy(np.ascontiguousarray(x)).to(f"cuda:{local}") for x in kb.arrays()]
     kd = KKTSystem(N, n, m, *dev)
     lam = torch.empty((B, (N + 1) * n), dtype=torch.float64, device=f"cuda:{local}")
@@ -373,9 +400,12 @@ def nmpc_batch_throughput(api, torch, local, B=4096, N=32, n=2, m=1, reps=5):
     path = ctx.last_path()
     ctx.close()
     ms = e0.elapsed_time(e1) / reps
-    return {"systems_per_s": B / (ms * 1e-3), "ms_per_batch": ms, "batch": B, "knots": N + 1,
-            "nx": n, "nu": m, "kernel": PATHS.get(path, str(path)),
-            "iters_mean": float(np.mean([r.iterations for r in reports]))}
+    out = {"systems_per_s": B / (ms * 1e-3), "ms_per_batch": ms, "batch": B, "knots": N + 1,
+           "nx": n, "nu": m, "kernel": PATHS.get(path, str(path)),
+           "iters_mean": float(np.mean([r.iterations for r in reports]))}
+    if keep:
+        out.update(_lam=lam.cpu().numpy(), _reports=reports, _kkt=kb)
+    return out
 
 
 def gpu_single(api, kk, kind, eps, dtype=np.float64, reps=20, warm=5):
@@ -666,6 +696,17 @@ def run_b200(a, world, rank, local):
             latency["nmpc_batch_n2"] = nmpc_batch_throughput(api, torch, local)
         except Exception as exc:
             latency["nmpc_batch_n2"] = {"error": str(exc)[:200]}
+        # off-BASELINE shapes: quadrotor-like n12 m4 and n7 m2
+        c4_tf = B * algorithmic(N, n, m, float(np.mean(iters)))["f_full"] / (
+            elapsed_ms / a.steps * 1e-3) / 1e12
+        shapes = {}
+        for (sn, sm_) in ((12, 4), (7, 2)):
+            try:
+                shapes[f"n{sn}_m{sm_}_K{N + 1}"] = shape_batch(api, torch, local, B, N, sn, sm_,
+                                                               c4_tflops=c4_tf)
+            except Exception as exc:
+                shapes[f"n{sn}_m{sm_}_K{N + 1}"] = {"error": str(exc)[:200]}
+        latency["off_baseline_shapes"] = shapes
 
     # ---- reconstruct_primal on the same batch
     primal = None
