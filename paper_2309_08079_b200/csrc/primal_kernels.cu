@@ -6,12 +6,18 @@
 //   dx_N = Q_N^-1 (-(q_N + lambda_N))
 // into dz = [x_0, u_0, x_1, u_1, ..., x_N].
 //
-// One warp per (system, knot, block): block 0 = the state solve, block 1 =
-// the control solve. The reference solves with Eigen's LDLT (never throws);
-// this kernel factors the block unpivoted as L D L' (same solution as the
-// reference's for the SPD cost blocks, and like it no error path), lane i
-// owning row i, the tile and the right-hand side in shared memory.
+// The reference solves with Eigen's LDLT (never throws); these kernels factor
+// each block unpivoted as L D L' (same solution as the reference's for the SPD
+// cost blocks, and like it no error path). Three variants:
+//   k_reconstruct_primal_bulk<14, 7> (fp64 batches of the c4 shape): CTAs of
+//     16 consecutive knot tasks whose operands arrive as bulk TMA streams,
+//     8-lane groups with two rows per lane (the bandwidth-bound path);
+//   k_reconstruct_primal_hw (other compiled shapes): one half-warp per task;
+//   k_reconstruct_primal (any n, m <= 32): one warp per (system, knot, block),
+//     block 0 = the state solve, block 1 = the control solve.
 #include "kernels.h"
+
+#include <cstdlib>
 
 namespace b2p {
 namespace {
@@ -255,6 +261,269 @@ __global__ void __launch_bounds__(16 * kPrHw) k_reconstruct_primal_hw(PrimalPara
     if (l < MB) dz[NB + l] = rhs;
   }
 }
+// ---------------------------------------------------------------------------
+// 8-lane group solves for the streaming batch path: a group owns one knot
+// task — the state solve of (system, k) with lane l < n/2 holding rows l and
+// l + n/2, or the control solve with lane l < m holding row l — so every
+// broadcast operand of the factorisation (the pivot row prefix) serves two
+// rows, and a warp carries four tasks. Same unpivoted L D L' arithmetic per
+// row as hw_ldlt_solve.
+
+__device__ __forceinline__ double recip(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ float recip(float x) { return __frcp_rn(x); }
+
+// D x = rhs on an 8-lane group, rows l and l + H of a D x D SPD block (D = 2H):
+// a0, a1 the rows, r0, r1 the right-hand sides (out: the solution rows).
+template <class T, int D>
+__device__ __forceinline__ void g8x2_ldlt_solve(T (&a0)[D], T (&a1)[D], T& r0, T& r1, T* Lt, int l) {
+  constexpr int H = D / 2;
+  const bool act = l < H;
+  const int lr = act ? l : H - 1;
+  T d0 = T(1), d1 = T(1);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    T s0 = T(0), s1 = a1[k];
+    if (k < H) s0 = a0[k];
+#pragma unroll
+    for (int q = 0; q < k; ++q) {
+      const T v = Lt[k * D + q];
+      if (k < H) s0 -= a0[q] * v;
+      s1 -= a1[q] * v;
+    }
+    const T dk = __shfl_sync(0xffffffffu, k < H ? s0 : s1, k < H ? k : k - H, 8);
+    const T rk = recip(dk);  // IEEE reciprocal: bitwise T(1) / dk
+    if (k < H) {
+      if (lr == k) d0 = dk;
+      if (act && lr > k) {
+        Lt[lr * D + k] = s0;
+        a0[k] = s0 * rk;
+      }
+    }
+    if (lr + H == k) d1 = dk;
+    if (act && lr + H > k) {
+      Lt[(lr + H) * D + k] = s1;
+      a1[k] = s1 * rk;
+    }
+    __syncwarp();
+  }
+  // L y = b (unit lower, column sweep), z = y / d
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    const T yq = __shfl_sync(0xffffffffu, q < H ? r0 : r1, q < H ? q : q - H, 8);
+    if (lr > q) r0 -= a0[q] * yq;
+    if (lr + H > q) r1 -= a1[q] * yq;
+  }
+  r0 = r0 / d0;
+  r1 = r1 / d1;
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      Lt[lr * D + q] = (q < lr) ? a0[q] : T(0);
+      Lt[(lr + H) * D + q] = (q < lr + H) ? a1[q] : T(0);
+    }
+  }
+  __syncwarp();
+  // L' x = z (transposed sweep through the unit-lower rows)
+#pragma unroll
+  for (int j = D - 1; j >= 0; --j) {
+    const T xj = __shfl_sync(0xffffffffu, j < H ? r0 : r1, j < H ? j : j - H, 8);
+    if (lr < j) r0 -= Lt[j * D + lr] * xj;
+    if (lr + H < j) r1 -= Lt[j * D + lr + H] * xj;
+  }
+}
+
+// the same on one row per lane (D <= 8; the control solve)
+template <class T, int D>
+__device__ __forceinline__ void g8_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l) {
+  const int lr = l < D ? l : D - 1;
+  T dl = T(1);
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    T s = a[k];
+#pragma unroll
+    for (int q = 0; q < k; ++q) s -= a[q] * Lt[k * D + q];
+    const T dk = __shfl_sync(0xffffffffu, s, k, 8);
+    const T rk = recip(dk);  // IEEE reciprocal: bitwise T(1) / dk
+    if (lr == k) dl = dk;
+    if (l < D && lr > k) {
+      Lt[lr * D + k] = s;
+      a[k] = s * rk;
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    const T yq = __shfl_sync(0xffffffffu, rhs, q, 8);
+    if (lr > q) rhs -= a[q] * yq;
+  }
+  rhs = rhs / dl;
+  if (l < D) {
+#pragma unroll
+    for (int q = 0; q < D; ++q) Lt[lr * D + q] = (q < lr) ? a[q] : T(0);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = D - 1; j >= 0; --j) {
+    const T xj = __shfl_sync(0xffffffffu, rhs, j, 8);
+    if (lr < j) rhs -= Lt[j * D + lr] * xj;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Streaming variant: a CTA owns 16 consecutive knot tasks of one kind and
+// brings their operands in with bulk asynchronous copies (TMA, one mbarrier):
+// consecutive tasks' Q_k / A_k / q_k / lambda_k blocks are contiguous in the
+// b2p_kkt layout, so the CTA's HBM reads are four long sequential streams
+// instead of per-lane row loads. The 8-lane groups then solve from shared
+// memory (Q_k's block doubles as its L tile).
+constexpr int kBulkTasks = 16;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+
+template <class T, int NB, int MB>
+__global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(PrimalParams<T> p) {
+  constexpr int H = NB / 2, NN = NB * NB;
+  extern __shared__ __align__(16) unsigned char praw[];
+  T* sm = reinterpret_cast<T*>(praw);
+  __shared__ __align__(8) unsigned long long mbar;
+  const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(&mbar));
+  const int grp = threadIdx.x >> 3, l = threadIdx.x & 7;
+  const int N = p.N, K = N + 1;
+  const long long nx = static_cast<long long>(p.B) * K, nu = static_cast<long long>(p.B) * N;
+  const long long nsc = (nx + kBulkTasks - 1) / kBulkTasks;  // state CTAs come first
+  const size_t pd = static_cast<size_t>(K) * NB + static_cast<size_t>(N) * MB;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (static_cast<long long>(blockIdx.x) < nsc) {
+    // ---- state solves: tasks t = t0 .. t0 + nt - 1, t = sys K + k
+    const long long t0 = static_cast<long long>(blockIdx.x) * kBulkTasks;
+    const int nt = static_cast<int>(nx - t0 < kBulkTasks ? nx - t0 : kBulkTasks);
+    // A blocks: a(t) = t - sys(t) for k < N; contiguous over the range
+    const long long sys0 = t0 / K, k0 = t0 % K;
+    const long long a_lo = k0 < N ? t0 - sys0 : t0 + 1 - (sys0 + 1);
+    const long long t1 = t0 + nt - 1, sys1 = t1 / K, k1 = t1 % K;
+    const long long a_hi = k1 < N ? t1 - sys1 : t1 - 1 - sys1;  // inclusive
+    const int na = static_cast<int>(a_hi >= a_lo ? a_hi - a_lo + 1 : 0);
+    const int nl = static_cast<int>((nx - t0) < nt + 1 ? (nx - t0) : nt + 1);  // lambda blocks
+    T* sQ = sm;                              // [16][NN] (then the L tiles)
+    T* sA = sQ + kBulkTasks * NN;            // [16][NN]
+    T* sq = sA + kBulkTasks * NN;            // [16][NB]
+    T* sl = sq + kBulkTasks * NB;            // [17][NB]
+    if (threadIdx.x == 0) {
+      const unsigned bq = static_cast<unsigned>(sizeof(T) * nt * NN), ba = static_cast<unsigned>(sizeof(T) * na * NN);
+      const unsigned bv = static_cast<unsigned>(sizeof(T) * nt * NB), bl = static_cast<unsigned>(sizeof(T) * nl * NB);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bq + ba + bv + bl) : "memory");
+      bulk_g2s(sQ, p.Q + static_cast<size_t>(t0) * NN, bq, mb);
+      if (na) bulk_g2s(sA, p.A + static_cast<size_t>(a_lo) * NN, ba, mb);
+      bulk_g2s(sq, p.q + static_cast<size_t>(t0) * NB, bv, mb);
+      bulk_g2s(sl, p.lambda + static_cast<size_t>(t0) * NB, bl, mb);
+    }
+    {
+      unsigned done = 0;
+      while (!done)
+        asm volatile("{\n.reg .pred q;\nmbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0;\nselp.u32 %0, 1, 0, q;\n}\n"
+                     : "=r"(done) : "r"(mb) : "memory");
+    }
+    const bool tv = grp < nt;
+    const int j = tv ? grp : nt - 1;  // groups past the range duplicate the last task, store nothing
+    const long long t = t0 + j;
+    const int sys = static_cast<int>(t / K), k = static_cast<int>(t % K);
+    const int lr = l < H ? l : H - 1;
+    T* Qb = sQ + static_cast<size_t>(j) * NN;
+    T a0[NB], a1[NB];
+#pragma unroll
+    for (int c = 0; c < NB; c += 2) {
+      const double2 u = *reinterpret_cast<const double2*>(Qb + lr * NB + c);
+      const double2 v = *reinterpret_cast<const double2*>(Qb + (lr + H) * NB + c);
+      a0[c] = u.x; a0[c + 1] = u.y; a1[c] = v.x; a1[c + 1] = v.y;
+    }
+    T at0 = T(0), at1 = T(0);
+    if (k < N) {  // (A_k' lambda_{k+1})_r = sum_c A_k(c, r) lambda_{k+1, c}
+      const T* Ab = sA + static_cast<size_t>(t - sys - a_lo) * NN;
+      const T* l1 = sl + static_cast<size_t>(j + 1) * NB;
+#pragma unroll
+      for (int c = 0; c < NB; c += 2) {
+        const double2 lv = *reinterpret_cast<const double2*>(l1 + c);
+        at0 += Ab[c * NB + lr] * lv.x;
+        at1 += Ab[c * NB + lr + H] * lv.x;
+        at0 += Ab[(c + 1) * NB + lr] * lv.y;
+        at1 += Ab[(c + 1) * NB + lr + H] * lv.y;
+      }
+    }
+    const T* qk = sq + static_cast<size_t>(j) * NB;
+    const T* lk = sl + static_cast<size_t>(j) * NB;
+    T r0 = -(qk[lr] + lk[lr] - at0);
+    T r1 = -(qk[lr + H] + lk[lr + H] - at1);
+    // duplicates work in place on their own copy? no: they share the last
+    // task's block, so they factor in a scratch tile instead
+    T* Lt = tv ? Qb : sA + static_cast<size_t>(kBulkTasks - 1 - grp) * NN;
+    __syncthreads();  // every group has its rows; A blocks consumed (duplicates' scratch)
+    g8x2_ldlt_solve<T, NB>(a0, a1, r0, r1, Lt, l);
+    if (tv && l < H) {
+      T* dz = p.dz + static_cast<size_t>(sys) * pd + static_cast<size_t>(k) * (NB + MB);
+      dz[lr] = r0;
+      dz[lr + H] = r1;
+    }
+  } else {
+    // ---- control solves: tasks u = u0 .. u0 + nt - 1, u = sys N + k
+    const long long u0 = (static_cast<long long>(blockIdx.x) - nsc) * kBulkTasks;
+    if (MB == 0 || u0 >= nu) return;
+    const int nt = static_cast<int>(nu - u0 < kBulkTasks ? nu - u0 : kBulkTasks);
+    // lambda_{k+1} blocks: index (u + sys + 1) over the range (contiguous)
+    const long long s0 = u0 / N, s1 = (u0 + nt - 1) / N;
+    const long long l_lo = u0 + s0 + 1, l_hi = u0 + nt - 1 + s1 + 1;
+    const int nl = static_cast<int>(l_hi - l_lo + 1);
+    T* sB = sm;                              // [16][NB MB]
+    T* sl = sB + kBulkTasks * NB * MB;       // [<= 16 + #systems][NB]
+    T* sR = sl + (kBulkTasks + 2 + kBulkTasks / (N > 0 ? N : 1)) * NB;  // [16][MB MB] (plain loads)
+    if (threadIdx.x == 0) {
+      const unsigned bb = static_cast<unsigned>(sizeof(T) * nt * NB * MB), bl = static_cast<unsigned>(sizeof(T) * nl * NB);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bb + bl) : "memory");
+      bulk_g2s(sB, p.B_ + static_cast<size_t>(u0) * NB * MB, bb, mb);
+      bulk_g2s(sl, p.lambda + static_cast<size_t>(l_lo) * NB, bl, mb);
+    }
+    for (int i = threadIdx.x; i < nt * MB * MB; i += 8 * kBulkTasks)
+      sR[i] = __ldg(p.R + static_cast<size_t>(u0) * MB * MB + i);
+    __syncthreads();
+    {
+      unsigned done = 0;
+      while (!done)
+        asm volatile("{\n.reg .pred q;\nmbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0;\nselp.u32 %0, 1, 0, q;\n}\n"
+                     : "=r"(done) : "r"(mb) : "memory");
+    }
+    const bool tv = grp < nt;
+    const int j = tv ? grp : nt - 1;
+    const long long u = u0 + j;
+    const int sys = static_cast<int>(u / N), k = static_cast<int>(u % N);
+    const int lr = l < MB ? l : MB - 1;
+    T a[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) a[c] = sR[j * MB * MB + lr * MB + c];
+    const T* Bb = sB + static_cast<size_t>(j) * NB * MB;
+    const T* l1 = sl + static_cast<size_t>(u + sys + 1 - l_lo) * NB;
+    T bt = T(0);
+#pragma unroll
+    for (int c = 0; c < NB; c += 2) {
+      const double2 lv = *reinterpret_cast<const double2*>(l1 + c);
+      bt += Bb[c * MB + lr] * lv.x;
+      bt += Bb[(c + 1) * MB + lr] * lv.y;
+    }
+    T rhs = -(__ldg(p.r + static_cast<size_t>(u) * MB + lr) - bt);
+    T* Lt = sR + static_cast<size_t>(kBulkTasks) * MB * MB + grp * MB * MB;  // private scratch
+    g8_ldlt_solve<T, MB>(a, rhs, Lt, l);
+    if (tv && l < MB)
+      p.dz[static_cast<size_t>(sys) * pd + static_cast<size_t>(k) * (NB + MB) + NB + lr] = rhs;
+  }
+}
 }  // namespace
 
 template <class T>
@@ -267,8 +536,24 @@ cudaError_t launch_reconstruct_primal(const PrimalParams<T>& p, cudaStream_t st)
     kern<<<static_cast<unsigned>(grid), 16 * kPrHw, 0, st>>>(p);
     return cudaGetLastError();
   };
+  auto bulk_launch = [&](auto kern, int nb, int mbk) {
+    const long long nx = static_cast<long long>(p.B) * (p.N + 1);
+    const long long nu = static_cast<long long>(p.B) * p.N;
+    const long long grid = (nx + kBulkTasks - 1) / kBulkTasks + (nu + kBulkTasks - 1) / kBulkTasks;
+    const size_t st_b = sizeof(T) * (2 * kBulkTasks * nb * nb + (2 * kBulkTasks + 1) * nb);
+    const size_t ct_b = sizeof(T) * (kBulkTasks * nb * mbk + (kBulkTasks + 2 + kBulkTasks) * nb +
+                                     2 * kBulkTasks * mbk * mbk);
+    const size_t smem = st_b > ct_b ? st_b : ct_b;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(grid), 8 * kBulkTasks, smem, st>>>(p);
+    return cudaGetLastError();
+  };
   if (tasks / kPrHw < 0x7fffffffLL) {
     if constexpr (sizeof(T) == 8) {
+      if (p.n == 14 && p.m == 7 && !std::getenv("B2P_PRIMAL_HW"))
+        return bulk_launch(k_reconstruct_primal_bulk<T, 14, 7>, 14, 7);
       if (p.n == 14 && p.m == 7) return hw_launch(k_reconstruct_primal_hw<T, 14, 7>);
     } else {
       if (p.n == 12 && p.m == 4) return hw_launch(k_reconstruct_primal_hw<T, 12, 4>);

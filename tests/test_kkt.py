@@ -81,11 +81,14 @@ def test_b200_matches_oracle_at_baseline_shapes(orc, shape):
 
 
 @pytest.mark.gpu
-def test_b200_batched_device_matches_single(orc):
+@pytest.mark.parametrize("Bn,N", [(6, 31), (7, 20), (3, 0), (5, 1), (41, 9)])
+def test_b200_batched_device_matches_single(orc, Bn, N):
+    # ragged horizons: the streaming kernel's 16-task CTAs straddle system
+    # boundaries (K = 21, 10) and the terminal knot (N = 0, 1)
     import torch
     import paper_2309_08079_b200.api as api
     api.require_device()
-    Bn, N, n, m = 6, 31, 14, 7
+    n, m = 14, 7
     kb = api.random_kkt_batch(500, Bn, N, n, m)
     lam = np.stack([orc.solve(kb.system(i)).lambda_ for i in range(Bn)])
     dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in kb.arrays()]
