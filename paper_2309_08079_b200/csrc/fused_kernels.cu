@@ -161,7 +161,9 @@ __host__ __device__ inline size_t fused_slot_stride(int K, int n, int m, bool ke
 // (R^-1 tiles and the slot use MB; EXM: m == MB exactly, else the runtime
 // p.m_rt <= MB with identity-padded R and zero-padded B, r — the pad terms add
 // exact zeros after the real ones, so every sum equals the unpadded one).
-template <class T, int NB, int MB, int R, bool EXM>
+// TM: the B2P_PHASE_TIMING build (globaltimer / SM-clock stamps); the
+// production instantiation carries no stamp code at all.
+template <class T, int NB, int MB, int R, bool EXM, bool TM>
 __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   static_assert(sizeof(T) == 8 && NB % 2 == 0 && NB <= 16 && MB <= 8,
                 "one-CTA kernel: fp64, even n <= 16, m <= 8");
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     const T* x0 = p.x0 + static_cast<size_t>(sys) * NB;
 
     __syncthreads();  // previous system's PCG is done with shared memory
-    unsigned long long* tm = (p.timing && tid == 0) ? p.timing + static_cast<size_t>(sys) * 16 : nullptr;
+    unsigned long long* tm = (TM && p.timing && tid == 0) ? p.timing + static_cast<size_t>(sys) * 16 : nullptr;
     if (tm) tm[0] = gtimer();
     if (tid == 0) s_err = 0x7fffffff;
 
@@ -1121,7 +1123,10 @@ cudaError_t launch_fused(const FusedParams<T>& p, int n, int m, int grid, cudaSt
       constexpr int NB = decltype(nb)::value, MB = decltype(mb)::value;
       constexpr bool EXM = decltype(exm)::value;
       const size_t smem = fused_smem_bytes<T, NB, MB>(q.K);
-      auto kern = q.K <= kHalfWarps ? k_fused_cta<T, NB, MB, 1, EXM> : k_fused_cta<T, NB, MB, 2, EXM>;
+      auto kern = q.timing ? (q.K <= kHalfWarps ? k_fused_cta<T, NB, MB, 1, EXM, true>
+                                                : k_fused_cta<T, NB, MB, 2, EXM, true>)
+                           : (q.K <= kHalfWarps ? k_fused_cta<T, NB, MB, 1, EXM, false>
+                                                : k_fused_cta<T, NB, MB, 2, EXM, false>);
       err = ensure_max_smem(kern, smem);
       if (err == cudaSuccess) {
         kern<<<grid, kThreads, smem, st>>>(q);
