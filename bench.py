@@ -696,11 +696,12 @@ def run_b200(a, world, rank, local):
             latency["nmpc_batch_n2"] = nmpc_batch_throughput(api, torch, local)
         except Exception as exc:
             latency["nmpc_batch_n2"] = {"error": str(exc)[:200]}
-        # off-BASELINE shapes: quadrotor-like n12 m4 and n7 m2
+        # off-BASELINE shapes: quadrotor-like n12 m4, n7 m2 and
+        # odd n13 m7 (one-CTA kernel on an identity-padded n + 1)
         c4_tf = B * algorithmic(N, n, m, float(np.mean(iters)))["f_full"] / (
             elapsed_ms / a.steps * 1e-3) / 1e12
         shapes = {}
-        for (sn, sm_) in ((12, 4), (7, 2)):
+        for (sn, sm_) in ((12, 4), (7, 2), (13, 7)):
             try:
                 shapes[f"n{sn}_m{sm_}_K{N + 1}"] = shape_batch(api, torch, local, B, N, sn, sm_,
                                                                c4_tflops=c4_tf)

@@ -479,6 +479,33 @@ constexpr int kErrOk = 0x7f7f7f7f;
 // dz_dev (nullable): the one-CTA and small-block kernels also run the PPCG
 // finish (reconstruct_primal) in their epilogue; returns whether dz was
 // produced (else the caller launches the primal kernel).
+// out[b] (ro x co) <- in[b] (ri x ci): copy the common top-left part, fill the
+// rest with zeros (diag: ones on the diagonal). Pads odd-n state blocks to
+// n + 1 for the one-CTA kernel (identity Q pad, zero A / B / vector pads) and
+// crops lambda back.
+template <class T>
+__global__ void k_reblock(const T* __restrict__ in, T* __restrict__ out, long long nblocks, int ri,
+                          int ci, int ro, int co, int diag) {
+  const long long total = nblocks * ro * co;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = e / (ro * co);
+    const int i = static_cast<int>((e / co) % ro), j = static_cast<int>(e % co);
+    out[e] = (i < ri && j < ci) ? in[b * ri * ci + static_cast<long long>(i) * ci + j]
+                                : ((diag && i == j) ? T(1) : T(0));
+  }
+}
+template <class T>
+void reblock(const void* in, void* out, long long nblocks, int ri, int ci, int ro, int co, int diag,
+             cudaStream_t st) {
+  const long long total = nblocks * ro * co;
+  if (total <= 0) return;
+  const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 4096));
+  k_reblock<T><<<grid, 256, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(out), nblocks, ri,
+                                      ci, ro, co, diag);
+  CK(cudaGetLastError());
+}
+
 template <class T>
 bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, int kind,
                        int order, const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
@@ -641,6 +668,85 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     CK(launch_fc<T>(f, fcG, max_clusters, st));
     c->launches++;
     c->last_path = 2;
+    c->phases = time_it;
+    if (time_it) CK(cudaEventRecord(c->ev1, st));
+    return false;
+  }
+  // Odd n in [9, 15] on the one-CTA kernel: the state dimension padded to n + 1
+  // (Q with an identity pad, A / B / q / e / x pads zero). Every pad entry of
+  // S, gamma, theta^-1 and of every PCG vector is then exactly zero, so the
+  // real rows follow the unpadded recurrence (the dot products only gain
+  // exact zero terms); lambda is cropped back.
+  const bool pad_ok = !drift && !dz_dev && sizeof(T) == 8 && (n & 1) && n >= 9 && n + 1 <= 16 &&
+                      env_int("B2P_FUSED", 1) && env_int("B2P_PAD", 1) &&
+                      fused_supported<T>(K, n + 1, k->m, kind);
+  if (pad_ok) {
+    const int np = n + 1, m = k->m, N = K - 1;
+    const long long Bl = B;
+    const size_t eQ = static_cast<size_t>(K) * np * np, eq = static_cast<size_t>(K) * np,
+                 eA = static_cast<size_t>(N) * np * np, eB = static_cast<size_t>(N) * np * m,
+                 ee = static_cast<size_t>(N) * np;
+    const size_t per = eQ + eq + eA + eB + ee + 2 * np;
+    T* w = static_cast<T*>(ws_get(c, tag + "pad_kkt", sizeof(T) * per * B + 256));
+    T *Qp = w, *qp = Qp + eQ * B, *Ap = qp + eq * B, *Bp = Ap + eA * B, *ep = Bp + eB * B,
+      *xsp = ep + ee * B, *x0p = xsp + static_cast<size_t>(np) * B;
+    reblock<T>(kv.Q, Qp, Bl * K, n, n, np, np, 1, st);
+    reblock<T>(kv.q, qp, Bl * K, n, 1, np, 1, 0, st);
+    reblock<T>(kv.A, Ap, Bl * N, n, n, np, np, 0, st);
+    reblock<T>(kv.B, Bp, Bl * N, n, m, np, m, 0, st);
+    reblock<T>(kv.e, ep, Bl * N, n, 1, np, 1, 0, st);
+    reblock<T>(kv.x_s, xsp, Bl, n, 1, np, 1, 0, st);
+    reblock<T>(kv.x0, x0p, Bl, n, 1, np, 1, 0, st);
+    T* lamp = static_cast<T*>(ws_get(c, tag + "pad_lam", sizeof(T) * B * K * np));
+    T* l0p = nullptr;
+    if (lambda0) {
+      l0p = static_cast<T*>(ws_get(c, tag + "pad_l0", sizeof(T) * B * K * np));
+      reblock<T>(lambda0, l0p, Bl * K, n, 1, np, 1, 0, st);
+    }
+    const int grid = std::max(1, std::min(B, c->sm_count));
+    FusedParams<T> f{};
+    f.B = B;
+    f.K = K;
+    f.kind = kind;
+    f.Q = Qp;
+    f.q = qp;
+    f.R = static_cast<const T*>(kv.R);
+    f.r = static_cast<const T*>(kv.r);
+    f.A = Ap;
+    f.Bm = Bp;
+    f.e = ep;
+    f.x_s = xsp;
+    f.x0 = x0p;
+    f.slot = static_cast<T*>(
+        ws_get(c, tag + "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, np, m, false)));
+    f.lambda0 = l0p;
+    f.lambda_out = lamp;
+    f.errkey = errkey;
+    f.out = outs_dev;
+    f.trace = trace_dev;
+    f.trace_cap = trace_cap;
+    f.epsilon = cfg ? cfg->epsilon : 1e-4;
+    const int mi = cfg ? cfg->max_iter : 0;
+    f.max_iter = mi > 0 ? mi : static_cast<int>(D);  // the unpadded dimension (resolve_max_iter)
+    if (time_it) {
+      if (!c->accounting) c->pool_used = 0;
+      if (c->pool_used + 3 > c->pool.size())
+        for (int q = 0; q < 3; ++q) {
+          cudaEvent_t e;
+          CK(cudaEventCreate(&e));
+          c->pool.push_back(e);
+        }
+      c->ev0 = c->pool[c->pool_used];
+      c->ev2 = c->pool[c->pool_used + 1];
+      c->ev1 = c->pool[c->pool_used + 2];
+      c->pool_used += 3;
+      CK(cudaEventRecord(c->ev0, st));
+      CK(cudaEventRecord(c->ev2, st));
+    }
+    CK(launch_fused<T>(f, np, m, grid, st));
+    reblock<T>(lamp, lambda_out, Bl * K, np, 1, n, 1, 0, st);
+    c->launches += 2 + (lambda0 ? 1 : 0) + 7;
+    c->last_path = 1;
     c->phases = time_it;
     if (time_it) CK(cudaEventRecord(c->ev1, st));
     return false;

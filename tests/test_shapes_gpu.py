@@ -101,3 +101,47 @@ def test_single_solve_warm_start_cap_errors_and_finish(api, orc):
     bad.R[40] = -np.eye(4)
     with pytest.raises(RuntimeError, match="build_schur: R at knot 40 is not positive definite"):
         api.solve(bad)
+
+
+ODD = [(64, 13, 7), (40, 11, 3), (33, 9, 2), (21, 15, 8), (2, 13, 4)]
+
+
+@pytest.mark.parametrize("K,n,m", ODD)
+def test_odd_n_padded_one_cta_matches_oracle(api, orc, env, K, n, m):
+    """Odd n in [9, 15]: the one-CTA kernel on n + 1 with an identity-padded
+    state (pad rows of S, theta^-1 and every PCG vector stay exactly zero);
+    per-system iteration counts and lambda against the oracle."""
+    env["B2P_FC"] = "0"
+    B = 20
+    kb = api.random_kkt_batch(8600 + 7 * n + K, B, K - 1, n, m)
+    cfg = PcgConfig(epsilon=1e-8)
+    for kind in (PrecondKind.symmetric_stair, PrecondKind.stair, PrecondKind.block_jacobi):
+        lam, reps = api.solve_batched(kb, kind, 1, cfg)
+        assert api.context().last_path() == 1
+        _, lo, ro = orc.solve_batch(kb, kind, 1, cfg)
+        assert np.array_equal(reps.iterations, np.array([r.iterations for r in ro]))
+        assert np.array_equal(reps.converged, np.array([bool(r.converged) for r in ro]))
+        scale = np.maximum(1.0, np.abs(lo).max(axis=1))
+        assert (np.abs(lam - lo).max(axis=1) / scale).max() <= TOL64
+
+
+def test_odd_n_padded_single_warm_start_cap_and_errors(api, orc):
+    kkt = orc.random_kkt(8701, 47, 13, 5)
+    cfg = PcgConfig(epsilon=1e-8)
+    got = api.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    want = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    assert got.report.iterations == want.report.iterations
+    assert rel_inf_error(got.lambda_, want.lambda_) <= TOL64
+    warm = api.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg, lambda0=0.5 * want.lambda_)
+    ow = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg, lambda0=0.5 * want.lambda_)
+    assert warm.report.iterations == ow.report.iterations
+    assert rel_inf_error(warm.lambda_, ow.lambda_) <= TOL64
+    capped = api.solve(kkt, PrecondKind.symmetric_stair, cfg=PcgConfig(epsilon=1e-14, max_iter=3))
+    oc = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=PcgConfig(epsilon=1e-14, max_iter=3))
+    assert not capped.report.converged and capped.report.iterations == 3
+    assert rel_inf_error(capped.lambda_, oc.lambda_) <= TOL64
+    # non-PD Q at knot 5: the reference's message, knot index unchanged by the pad
+    bad = orc.random_kkt(8702, 47, 13, 5)
+    bad.Q[5] = -np.eye(13)
+    with pytest.raises(RuntimeError, match="build_schur: Q at knot 5 is not positive definite"):
+        api.solve(bad, PrecondKind.symmetric_stair, cfg=cfg)
