@@ -417,6 +417,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           const T* Bk = Bs + static_cast<size_t>(k) * nm;
           const T* Xk = sQi + static_cast<size_t>(k) * NN;
           const T* Xk1 = Xk + NN;
+          // e_k rows for gamma, issued first (their latency hides behind the
+          // tensor-core chains; lane (r, 0) owns rows r and r + 8)
+          T ek[2];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const int i = mt * 8 + fr;
+            ek[mt] = (fc == 0 && i < NB) ? __ldg(es + k * NB + i) : T(0);
+          }
           // operand fragments: A (row r, col c), B (row c, col r)
           T af[2][4], bf[2][2], xf[2][4], rf[2];
 #pragma unroll
@@ -510,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
                   brr += ((EXM || q < m) ? __ldg(Bk + i * m + q) : T(0)) * srr[k * 8 + q];
               }
               const T zeta = (-aqq - brr) + sqq[(k + 1) * 16 + i];
-              const T g = -(-__ldg(es + k * NB + i) + zeta);
+              const T g = -(-ek[mt] + zeta);
               gG[static_cast<size_t>(b) * NB + i] = g;
               if (p.form_only) p.gamma_out[(static_cast<size_t>(sys) * K + b) * NB + i] = g;
             }
