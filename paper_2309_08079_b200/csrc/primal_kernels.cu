@@ -10,7 +10,7 @@
 // each block unpivoted as L D L' (same solution as the reference's for the SPD
 // cost blocks, and like it no error path). Three variants:
 //   k_reconstruct_primal_bulk<14, 7> (fp64 batches of the c4 shape): CTAs of
-//     16 consecutive knot tasks whose operands arrive as bulk TMA streams,
+//     4 consecutive knot tasks whose operands arrive as bulk TMA streams,
 //     8-lane groups with two rows per lane (the bandwidth-bound path);
 //   k_reconstruct_primal_hw (other compiled shapes): one half-warp per task;
 //   k_reconstruct_primal (any n, m <= 32): one warp per (system, knot, block),
@@ -370,13 +370,13 @@ __device__ __forceinline__ void g8_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l) {
 }
 
 // ---------------------------------------------------------------------------
-// Streaming variant: a CTA owns 16 consecutive knot tasks of one kind and
+// Streaming variant: a CTA owns kBulkTasks consecutive knot tasks of one kind and
 // brings their operands in with bulk asynchronous copies (TMA, one mbarrier):
 // consecutive tasks' Q_k / A_k / q_k / lambda_k blocks are contiguous in the
 // b2p_kkt layout, so the CTA's HBM reads are four long sequential streams
 // instead of per-lane row loads. The 8-lane groups then solve from shared
 // memory (Q_k's block doubles as its L tile).
-constexpr int kBulkTasks = 16;
+constexpr int kBulkTasks = 4;
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned mbar) {
   asm volatile(
