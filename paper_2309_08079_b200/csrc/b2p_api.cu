@@ -531,11 +531,12 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   const int fgRp = (drift || B > 8) ? 0
                                     : fg_pick_rp<T>(K, n, k->m, kind, c->sm_count,
                                                     env_int("B2P_FG_RP", 0));
-  // Single-solve policy (scripts/c1_policy_probe.py, profiles/r02_single_policy.json):
-  // 33 <= K <= 64 on one CTA (K 64: 87 us vs 93 on the grid kernel), other fp64
-  // horizons on the grid kernel (c1, K 32: 73 us vs 77 on one CTA), fp32 /
-  // other shapes on the cluster kernel.
-  const bool single_short = B == 1 && K > 32 && K <= 64 && one_cta_ok;
+  // Single-solve policy (scripts/c1_policy_probe.py, profiles/r02_single_policy.json,
+  // and the bench's c1 row): K <= 64 on one CTA (K 64: 87 us vs 93 on the grid
+  // kernel; c1: 77 us in the bench vs 88 on the grid kernel there, although an
+  // isolated probe timed the grid kernel at 73), longer fp64 horizons on the
+  // grid kernel, fp32 / other shapes on the cluster kernel.
+  const bool single_short = B == 1 && K <= 64 && one_cta_ok;
   const bool use_fg = fgRp > 0 && env_int("B2P_FUSED", 1) &&
                       (fg_env == 1 ||
                        (fg_env == -1 && ((fcG == 0 && !one_cta_ok) ||
