@@ -49,3 +49,20 @@ st = torch.empty((2,), dtype=torch.int32, device="cuda")
 api.direct_solve_batched_device(kd, lam.data_ptr(), st.data_ptr(), 2)
 torch.cuda.synchronize()
 print("direct baseline", st.cpu().tolist())
+# round 2: several systems per CTA on the c4 kernel (next-system prefetch vs the
+# formation / theta^-1 tiles, D kept in place), the odd-n padded path and the
+# streaming reconstruct_primal kernel (CTAs straddling system boundaries)
+SAN_B = int(os.environ.get("SAN_B", "300"))
+kb = api.random_kkt_batch(14, SAN_B, 63, 14, 7)
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("batched one-CTA K64", SAN_B, api.context().last_path(), int(reps.iterations.sum()))
+kb = api.random_kkt_batch(15, 4, 20, 13, 5)
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("odd-n padded", api.context().last_path(), [x.iterations for x in reps])
+kb = api.random_kkt_batch(16, 7, 20, 14, 7)
+kd = KKTSystem(20, 14, 7, *[torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in kb.arrays()])
+lamd = torch.zeros((7, 21 * 14), dtype=torch.float64, device="cuda")
+dz = torch.empty((7, kb.primal_dim()), dtype=torch.float64, device="cuda")
+api.reconstruct_primal_batched_device(kd, lamd.data_ptr(), dz.data_ptr(), 7)
+torch.cuda.synchronize()
+print("streaming reconstruct_primal", float(dz.abs().sum()))
