@@ -738,16 +738,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       for (int c = 0; c < 2; ++c) {
         // row pr + H c of R_b = column pr + H c of L_{b+1} (padded stride LS:
         // the four quarter-warps read disjoint banks)
+        // (the missing neighbour blocks — L_0, R_{K-1} — are stored as exact
+        // zeros, so the block products need no edge selects)
         const T* Lc = sL + static_cast<size_t>(pbn) * LS + pr + H * c;
+        const bool rz = pbc + 1 >= K, lz = pbc == 0;
 #pragma unroll
-        for (int j = 0; j < NB; ++j) mrow[j] = Lc[j * NB];
+        for (int j = 0; j < NB; ++j) mrow[j] = rz ? T(0) : Lc[j * NB];
         tm::st_row<NB>(colR(c), mrow);
         const T* Lr = sL + static_cast<size_t>(pbc) * LS + (pr + H * c) * NB;
 #pragma unroll
         for (int j = 0; j < NB; j += 2) {
           const double2 v = *reinterpret_cast<const double2*>(Lr + j);
-          mrow[j] = v.x;
-          mrow[j + 1] = v.y;
+          mrow[j] = lz ? T(0) : v.x;
+          mrow[j + 1] = lz ? T(0) : v.y;
         }
         tm::st_row<NB>(colL(c), mrow);
       }
@@ -811,8 +814,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         T out = sd[c];
-        if (pbc > 0) out += sl[c];
-        if (pbc + 1 < K) out += sr[c];
+        out += sl[c];  // L_0 and R_{K-1} rows are exact zeros in TMEM
+        out += sr[c];
         y[c] = out;
       }
     };
@@ -861,8 +864,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         T v = rr[c];
-        if (pbc > 0) v -= sl[c];
-        if (pbc + 1 < K) v -= sr[c];
+        v -= sl[c];
+        v -= sr[c];
         if (pact) su[pbc * NB + pi + H * c] = v;
       }
       __syncwarp();
