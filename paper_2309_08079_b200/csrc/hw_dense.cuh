@@ -128,17 +128,15 @@ __device__ __forceinline__ T block_reduce(T v, T* red) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   // pairwise tree over the warp partials (fixed order: every thread gets the
-  // bit-identical sum; depth log2(#warps) instead of a #warps-long DADD chain)
+  // bit-identical sum; depth log2(#warps)): lane w holds partial w, level st
+  // adds lane w + st's value — lane 0 ends with ((t0+t1)+(t2+t3))+... — then
+  // broadcasts it (one shared load per lane instead of #warps)
   constexpr int NW = kThreads / 32;
-  T t[NW];
+  static_assert((NW & (NW - 1)) == 0 && NW <= 32, "power-of-two warp count");
+  T s = lane < NW ? red[lane] : T(0);
 #pragma unroll
-  for (int w = 0; w < NW; ++w) t[w] = red[w];
-#pragma unroll
-  for (int st = 1; st < NW; st <<= 1) {
-#pragma unroll
-    for (int w = 0; w + st < NW; w += 2 * st) t[w] += t[w + st];
-  }
-  return t[0];
+  for (int st = 1; st < NW; st <<= 1) s += __shfl_down_sync(FULL, s, st);
+  return __shfl_sync(FULL, s, 0);
 }
 
 // ---------------------------------------------------------------- PCG row products
