@@ -36,18 +36,14 @@ constexpr int kHalfWarps = kThreads / 16;
 using namespace hwd;
 
 // Formation-phase shared memory (elements): per-knot Q^-1 and the products
-// Q^-1 q, R^-1 r, then per-half-warp scratch tiles (R^-1 goes to the slot).
+// Q^-1 q, R^-1 r, then the 8-lane group tiles (R^-1 goes to the slot) whose
+// region ends with the D blocks the PCG reads in place, then the q_k.
 template <class T, int NB, int MB>
 struct FLayout {
-  static constexpr int LD = Odd<NB>::v;
-  static constexpr int LDM = Odd<MB>::v;
-  // tW: transposes / AQ / Lr tile; tX: L^-T tile, aliased by B R^-1; rd[16], v[16]
-  static constexpr int TX = NB * NB > 128 ? NB * NB : 128;  // >= two 8x8 R^-1 tiles
-  static constexpr int per_hw = NB * LD + TX + 32;
   // 8-lane group tiles of F1 (L^-T of Q_g, then the R_g^-1 tiles) and of the
   // theta^-1 pass: [max(n n, 2 MB MB)] | rd [16]
   static constexpr int g8_tile = (NB * NB > 2 * MB * MB ? NB * NB : 2 * MB * MB) + 16;
-  static constexpr int tiles0 = kHalfWarps * per_hw > 64 * g8_tile ? kHalfWarps * per_hw : 64 * g8_tile;
+  static constexpr int tiles0 = 64 * g8_tile;
   __host__ __device__ static int oQi(int) { return 0; }
   __host__ __device__ static int oqq(int K) { return K * NB * NB; }
   __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
@@ -171,7 +167,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using FL = FLayout<T, NB, MB>;
   constexpr int NN = NB * NB;
-  constexpr int LD = FL::LD, LDM = FL::LDM;
   const int K = p.K, N = K - 1;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -251,12 +246,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     if (tm) tm[0] = gtimer();
     if (tid == 0) s_err = 0x7fffffff;
 
-    T* hw = smem + FL::ohw(K) + static_cast<size_t>(h) * FL::per_hw;
-    T* tW = hw;
-    T* tX = tW + NB * LD;
-    T* tBR = tX;  // B R^-1 (stride LDM) is dead before the theta inverse needs tX
-    T* rd = tX + FL::TX;
-    const int lr = lact ? l : NB - 1;
     int fkey = 0x7fffffff;
 
     // ============================================================ F1: knots
