@@ -17,6 +17,7 @@
 //     block 0 = the state solve, block 1 = the control solve.
 #include "kernels.h"
 
+#include <cstdint>
 #include <cstdlib>
 
 namespace b2p {
@@ -269,7 +270,17 @@ __global__ void __launch_bounds__(16 * kPrHw) k_reconstruct_primal_hw(PrimalPara
 // rows, and a warp carries four tasks. Same unpivoted L D L' arithmetic per
 // row as hw_ldlt_solve.
 
-__device__ __forceinline__ double recip(double x) { return __drcp_rn(x); }
+// reciprocal of a (positive, normal) pivot: the hardware approximation and two
+// Newton steps (within an ulp of the IEEE reciprocal; the reference's LDLT
+// pivots differently anyway, parity is tolerance-pinned)
+__device__ __forceinline__ double recip(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 __device__ __forceinline__ float recip(float x) { return __frcp_rn(x); }
 
 // D x = rhs on an 8-lane group, rows l and l + H of a D x D SPD block (D = 2H):
@@ -395,25 +406,26 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
   const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(&mbar));
   const int grp = threadIdx.x >> 3, l = threadIdx.x & 7;
   const int N = p.N, K = N + 1;
-  const long long nx = static_cast<long long>(p.B) * K, nu = static_cast<long long>(p.B) * N;
-  const long long nsc = (nx + kBulkTasks - 1) / kBulkTasks;  // state CTAs come first
+  // 32-bit task indices (the launcher guarantees B K < 2^31)
+  const int nx = p.B * K, nu = p.B * N;
+  const int nsc = (nx + kBulkTasks - 1) / kBulkTasks;  // state CTAs come first
   const size_t pd = static_cast<size_t>(K) * NB + static_cast<size_t>(N) * MB;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(mb) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (static_cast<long long>(blockIdx.x) < nsc) {
+  if (static_cast<int>(blockIdx.x) < nsc) {
     // ---- state solves: tasks t = t0 .. t0 + nt - 1, t = sys K + k
-    const long long t0 = static_cast<long long>(blockIdx.x) * kBulkTasks;
-    const int nt = static_cast<int>(nx - t0 < kBulkTasks ? nx - t0 : kBulkTasks);
+    const int t0 = static_cast<int>(blockIdx.x) * kBulkTasks;
+    const int nt = nx - t0 < kBulkTasks ? nx - t0 : kBulkTasks;
     // A blocks: a(t) = t - sys(t) for k < N; contiguous over the range
-    const long long sys0 = t0 / K, k0 = t0 % K;
-    const long long a_lo = k0 < N ? t0 - sys0 : t0 + 1 - (sys0 + 1);
-    const long long t1 = t0 + nt - 1, sys1 = t1 / K, k1 = t1 % K;
-    const long long a_hi = k1 < N ? t1 - sys1 : t1 - 1 - sys1;  // inclusive
-    const int na = static_cast<int>(a_hi >= a_lo ? a_hi - a_lo + 1 : 0);
-    const int nl = static_cast<int>((nx - t0) < nt + 1 ? (nx - t0) : nt + 1);  // lambda blocks
+    const int sys0 = t0 / K;
+    const int a_lo = t0 - sys0;  // = a(t0), or a of the next task when k0 = N
+    const int t1 = t0 + nt - 1, sys1 = t1 / K, k1 = t1 - sys1 * K;
+    const int a_hi = k1 < N ? t1 - sys1 : t1 - 1 - sys1;  // inclusive
+    const int na = a_hi >= a_lo ? a_hi - a_lo + 1 : 0;
+    const int nl = (nx - t0) < nt + 1 ? (nx - t0) : nt + 1;  // lambda blocks
     T* sQ = sm;                              // [16][NN] (then the L tiles)
     T* sA = sQ + kBulkTasks * NN;            // [16][NN]
     T* sq = sA + kBulkTasks * NN;            // [16][NB]
@@ -435,8 +447,8 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     }
     const bool tv = grp < nt;
     const int j = tv ? grp : nt - 1;  // groups past the range duplicate the last task, store nothing
-    const long long t = t0 + j;
-    const int sys = static_cast<int>(t / K), k = static_cast<int>(t % K);
+    const int t = t0 + j;
+    const int sys = t / K, k = t - sys * K;
     const int lr = l < H ? l : H - 1;
     T* Qb = sQ + static_cast<size_t>(j) * NN;
     T a0[NB], a1[NB];
@@ -475,24 +487,39 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     }
   } else {
     // ---- control solves: tasks u = u0 .. u0 + nt - 1, u = sys N + k
-    const long long u0 = (static_cast<long long>(blockIdx.x) - nsc) * kBulkTasks;
+    const int u0 = (static_cast<int>(blockIdx.x) - nsc) * kBulkTasks;
     if (MB == 0 || u0 >= nu) return;
-    const int nt = static_cast<int>(nu - u0 < kBulkTasks ? nu - u0 : kBulkTasks);
+    const int nt = nu - u0 < kBulkTasks ? nu - u0 : kBulkTasks;
     // lambda_{k+1} blocks: index (u + sys + 1) over the range (contiguous)
-    const long long s0 = u0 / N, s1 = (u0 + nt - 1) / N;
-    const long long l_lo = u0 + s0 + 1, l_hi = u0 + nt - 1 + s1 + 1;
-    const int nl = static_cast<int>(l_hi - l_lo + 1);
+    const int s0 = u0 / N, s1 = (u0 + nt - 1) / N;
+    const int l_lo = u0 + s0 + 1, l_hi = u0 + nt - 1 + s1 + 1;
+    const int nl = l_hi - l_lo + 1;
     T* sB = sm;                              // [16][NB MB]
     T* sl = sB + kBulkTasks * NB * MB;       // [<= 16 + #systems][NB]
     T* sR = sl + (kBulkTasks + 2 + kBulkTasks / (N > 0 ? N : 1)) * NB;  // [16][MB MB] (plain loads)
+    // R_k (and r_k) blocks are 8-byte sized: bulk copies only where the range
+    // happens to be 16-byte aligned (always, inside whole batches with an even
+    // task count per CTA), plain loads otherwise
+    const T* Rg = p.R + static_cast<size_t>(u0) * MB * MB;
+    const unsigned br = static_cast<unsigned>(sizeof(T) * nt * MB * MB);
+    const bool r_bulk = ((reinterpret_cast<uintptr_t>(Rg) | br) & 15u) == 0;
+    T* sr_ = sR + static_cast<size_t>(2 * kBulkTasks) * MB * MB;  // [tasks][MB] r_k
+    const T* rg = p.r + static_cast<size_t>(u0) * MB;
+    const unsigned bv = static_cast<unsigned>(sizeof(T) * nt * MB);
+    const bool v_bulk = ((reinterpret_cast<uintptr_t>(rg) | bv) & 15u) == 0;
     if (threadIdx.x == 0) {
       const unsigned bb = static_cast<unsigned>(sizeof(T) * nt * NB * MB), bl = static_cast<unsigned>(sizeof(T) * nl * NB);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bb + bl) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb),
+                   "r"(bb + bl + (r_bulk ? br : 0u) + (v_bulk ? bv : 0u)) : "memory");
       bulk_g2s(sB, p.B_ + static_cast<size_t>(u0) * NB * MB, bb, mb);
       bulk_g2s(sl, p.lambda + static_cast<size_t>(l_lo) * NB, bl, mb);
+      if (r_bulk) bulk_g2s(sR, Rg, br, mb);
+      if (v_bulk) bulk_g2s(sr_, rg, bv, mb);
     }
-    for (int i = threadIdx.x; i < nt * MB * MB; i += 8 * kBulkTasks)
-      sR[i] = __ldg(p.R + static_cast<size_t>(u0) * MB * MB + i);
+    if (!r_bulk)
+      for (int i = threadIdx.x; i < nt * MB * MB; i += 8 * kBulkTasks) sR[i] = __ldg(Rg + i);
+    if (!v_bulk)
+      for (int i = threadIdx.x; i < nt * MB; i += 8 * kBulkTasks) sr_[i] = __ldg(rg + i);
     __syncthreads();
     {
       unsigned done = 0;
@@ -502,8 +529,8 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     }
     const bool tv = grp < nt;
     const int j = tv ? grp : nt - 1;
-    const long long u = u0 + j;
-    const int sys = static_cast<int>(u / N), k = static_cast<int>(u % N);
+    const int u = u0 + j;
+    const int sys = u / N, k = u - sys * N;
     const int lr = l < MB ? l : MB - 1;
     T a[MB];
 #pragma unroll
@@ -517,7 +544,7 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
       bt += Bb[c * MB + lr] * lv.x;
       bt += Bb[(c + 1) * MB + lr] * lv.y;
     }
-    T rhs = -(__ldg(p.r + static_cast<size_t>(u) * MB + lr) - bt);
+    T rhs = -(sr_[j * MB + lr] - bt);
     T* Lt = sR + static_cast<size_t>(kBulkTasks) * MB * MB + grp * MB * MB;  // private scratch
     g8_ldlt_solve<T, MB>(a, rhs, Lt, l);
     if (tv && l < MB)
@@ -542,7 +569,7 @@ cudaError_t launch_reconstruct_primal(const PrimalParams<T>& p, cudaStream_t st)
     const long long grid = (nx + kBulkTasks - 1) / kBulkTasks + (nu + kBulkTasks - 1) / kBulkTasks;
     const size_t st_b = sizeof(T) * (2 * kBulkTasks * nb * nb + (2 * kBulkTasks + 1) * nb);
     const size_t ct_b = sizeof(T) * (kBulkTasks * nb * mbk + (kBulkTasks + 2 + kBulkTasks) * nb +
-                                     2 * kBulkTasks * mbk * mbk);
+                                     2 * kBulkTasks * mbk * mbk + kBulkTasks * mbk) + 16;
     const size_t smem = st_b > ct_b ? st_b : ct_b;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -552,8 +579,8 @@ cudaError_t launch_reconstruct_primal(const PrimalParams<T>& p, cudaStream_t st)
   };
   if (tasks / kPrHw < 0x7fffffffLL) {
     if constexpr (sizeof(T) == 8) {
-      if (p.n == 14 && p.m == 7 && !std::getenv("B2P_PRIMAL_HW"))
-        return bulk_launch(k_reconstruct_primal_bulk<T, 14, 7>, 14, 7);
+      if (p.n == 14 && p.m == 7 && tasks < 0x7fffffffLL && !std::getenv("B2P_PRIMAL_HW"))
+        return bulk_launch(k_reconstruct_primal_bulk<T, 14, 7>, 14, 7);  // 32-bit task indices
       if (p.n == 14 && p.m == 7) return hw_launch(k_reconstruct_primal_hw<T, 14, 7>);
     } else {
       if (p.n == 12 && p.m == 4) return hw_launch(k_reconstruct_primal_hw<T, 12, 4>);
