@@ -44,21 +44,43 @@ struct FLayout {
   // theta^-1 pass: [max(n n, 2 MB MB)] | rd [16]
   static constexpr int g8_tile = (NB * NB > 2 * MB * MB ? NB * NB : 2 * MB * MB) + 16;
   static constexpr int tiles0 = 64 * g8_tile;
-  __host__ __device__ static int oQi(int) { return 0; }
-  __host__ __device__ static int oqq(int K) { return K * NB * NB; }
-  __host__ __device__ static int orr(int K) { return oqq(K) + K * 16; }
-  __host__ __device__ static int ohw(int K) { return orr(K) + (K - 1) * 8; }
+  static constexpr int ls = NB * NB + ((8 - (NB * NB) % 32) + 32) % 32;  // fused_ls(NB)
+  __host__ __device__ static constexpr int oQi(int) { return 0; }
+  __host__ __device__ static constexpr int oqq(int K) { return K * NB * NB; }
+  __host__ __device__ static constexpr int orr(int K) { return oqq(K) + K * 16; }
+  __host__ __device__ static constexpr int ohw(int K) { return orr(K) + (K - 1) * 8; }
   // The tile region also holds, at its end, the D blocks F2 leaves in place for
   // the PCG (theta_1..theta_63, D_0 = Q_0^-1 before them: oD); it is sized so
   // they clear the PCG's staged L (padded stride) and vectors below them.
-  __host__ __device__ static int tiles(int K) {
-    const int ls = NB * NB + ((8 - (NB * NB) % 32) + 32) % 32;  // fused_ls(NB)
+  __host__ __device__ static constexpr int tiles(int K) {
     const int need = K * ls + 3 * K * NB + 32 - ohw(K) + 64 * NB * NB;
     return tiles0 > need ? tiles0 : need;
   }
-  __host__ __device__ static int oD(int K) { return ohw(K) + tiles(K) - 64 * NB * NB; }
-  __host__ __device__ static int osq(int K) { return ohw(K) + tiles(K); }  // q_k
-  __host__ __device__ static int total(int K) { return osq(K) + K * NB; }
+  __host__ __device__ static constexpr int oD(int K) { return ohw(K) + tiles(K) - 64 * NB * NB; }
+  __host__ __device__ static constexpr int osq(int K) { return ohw(K) + tiles(K); }  // q_k
+  __host__ __device__ static constexpr int total(int K) { return osq(K) + K * NB; }
+  // PCG vectors p, t, u (+ the reduction words) after the staged L
+  __host__ __device__ static constexpr int osp(int K) { return K * ls; }
+  static constexpr size_t elems(int K) {
+    const size_t pcg = static_cast<size_t>(K) * (NB * NB + ls) + 3 * K * NB + 64;
+    return pcg > static_cast<size_t>(total(K)) ? pcg : static_cast<size_t>(total(K));
+  }
+  // horizon K fits: the theta^-1 pass's group tiles (groups < K + 3) stay
+  // clear of the D blocks F2 leaves in place (oD), and shared memory holds it
+  static constexpr bool fits(int K) {
+    return (K + 3) * g8_tile <= oD(K) && elems(K) * sizeof(T) + 64 <= 227 * 1024;
+  }
+  static constexpr int capacity(int kmax) {
+    for (int K = kmax; K >= 2; --K)
+      if (fits(K)) return K;
+    return 0;
+  }
+  // The kernel lays shared memory out for its largest horizon (kcap(R)), not
+  // for the launch's K: every region offset is a compile-time constant, so the
+  // PCG's per-thread addresses are one register plus immediates (a runtime-K
+  // layout had the compiler rematerialise them — S2R / LDC / IMAD — inside the
+  // solve loop: 10 % of the kernel's instructions).
+  static constexpr int kcap(int R) { return capacity(R == 1 ? 32 : 64); }
 };
 
 }  // namespace
@@ -180,17 +202,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   // region past `red`); sL: the L blocks at the padded stride LS.
   constexpr int LS = fused_ls(NB);
   T* sL = smem;                                 // [K][LS]  staging only
-  T* sp = smem + static_cast<size_t>(K) * LS;   // [K][NB]
-  T* st = sp + K * NB;
-  T* su = st + K * NB;
-  T* red = su + K * NB;                         // [32]
+  constexpr int KL = FL::kcap(R);  // the layout's horizon (>= K)
+  static_assert(KL >= 2, "no horizon fits the one-CTA layout");
+  T* sp = smem + FL::osp(KL);                   // [K][NB]
+  T* st = sp + KL * NB;
+  T* su = st + KL * NB;
+  T* red = su + KL * NB;                        // [32]
   // D_b rows stay where the formation left them: theta_b (b >= 1) at the end
   // of the tile region (F2), D_0 = Q_0^-1 just before (FLayout::oD)
-  T* sD = smem + FL::oD(K);                     // [K][NB][NB]  D row products
+  T* sD = smem + FL::oD(KL);                    // [K][NB][NB]  D row products
   // formation layout (aliases the PCG layout; phases are separated by barriers)
-  T* sQi = smem + FL::oQi(K);   // [K][NB][NB], column l written by lane l
-  T* sqq = smem + FL::oqq(K);   // [K][16]  Q_k^-1 q_k
-  T* srr = smem + FL::orr(K);   // [N][8]   R_k^-1 r_k
+  T* sQi = smem + FL::oQi(KL);   // [K][NB][NB], column l written by lane l
+  T* sqq = smem + FL::oqq(KL);   // [K][16]  Q_k^-1 q_k
+  T* srr = smem + FL::orr(KL);   // [N][8]   R_k^-1 r_k
   __shared__ int s_err;
   __shared__ __align__(8) unsigned long long s_mbar;  // TMA staging barrier
   __shared__ __align__(8) unsigned long long s_mbar2;  // next system's Q prefetch
@@ -253,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     // by the two block rows that use them (the reference recomputes them per
     // row, schur.cpp:49-51; same arithmetic). All Q_k arrive in one TMA bulk
     // copy (sQi) and are inverted in place; lanes read their rows from smem.
-    T* sq = smem + FL::osq(K);  // q_k of every knot (for Q_k^-1 q_k)
+    T* sq = smem + FL::osq(KL);  // q_k of every knot (for Q_k^-1 q_k)
     if (mst & 4u) {
       mbar_wait_bit(mbar2_addr, mst, 2u);  // prefetched during the previous PCG
     } else {
@@ -280,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       constexpr int H = NB / 2;
       const int g = tid >> 3, gl = tid & 7;
       const int glr = gl < H ? gl : H - 1;
-      T* gt = smem + FL::ohw(K) + static_cast<size_t>(g) * FL::g8_tile;
+      T* gt = smem + FL::ohw(KL) + static_cast<size_t>(g) * FL::g8_tile;
       const bool kv = g < K;
       const int kc = kv ? g : K - 1;
       // R_g row issued first: its L2 latency hides behind the Q_g inverse
@@ -391,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
             for (int j = 0; j < NB; ++j) {
               const T d = sQi[lane * NB + j];
-              smem[FL::oD(K) + lane * NB + j] = d;  // D_0 in place for the PCG
+              smem[FL::oD(KL) + lane * NB + j] = d;  // D_0 in place for the PCG
               if (p.form_only) {
                 p.S_out[static_cast<size_t>(sys) * K * 3 * nn + nn + lane * NB + j] = d;
                 p.theta_out[static_cast<size_t>(sys) * K * nn + lane * NB + j] =
@@ -563,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           // theta = (theta_raw + theta_raw')/2 (schur.cpp:67): the transposed
           // element (j, i) of lane (r, c)'s (i, j) = (8 mt + r, 8 nt + 2c + e)
           // sits in lane (2c + e, r / 2), tile (nt, mt), element r & 1
-          T* thb = smem + FL::oD(K) + static_cast<size_t>(b) * NN;  // = the PCG's D_b
+          T* thb = smem + FL::oD(KL) + static_cast<size_t>(b) * NN;  // = the PCG's D_b
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -611,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       const int bi = b == 0 ? 1 : (b < K ? b : K - 1);
       T* gt = smem + static_cast<size_t>(b) * FL::g8_tile;  // sQi region (dead)
       T a0[NB], a1[NB];
-      const T* Th = smem + FL::oD(K) + static_cast<size_t>(bi) * NN + glr * NB;
+      const T* Th = smem + FL::oD(KL) + static_cast<size_t>(bi) * NN + glr * NB;
 #pragma unroll
       for (int i = 0; i < NB; i += 2) {
         const double2 u = *reinterpret_cast<const double2*>(Th + i);
@@ -761,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
                        "r"(bq + bv)
                        : "memory");
           tma_copy_1d(sQi, p.Q + static_cast<size_t>(nsys) * K * nn, bq, mbar2_addr);
-          tma_copy_1d(smem + FL::osq(K), p.q + static_cast<size_t>(nsys) * K * NB, bv, mbar2_addr);
+          tma_copy_1d(smem + FL::osq(KL), p.q + static_cast<size_t>(nsys) * K * NB, bv, mbar2_addr);
         }
         mst |= 4u;
       }
@@ -1053,12 +1077,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 }
 
 template <class T, int NB, int MB>
-size_t fused_smem_bytes(int K) {
+size_t fused_smem_bytes(int K) {  // the layout of the instantiation K launches
   using FL = FLayout<T, NB, MB>;
-  const size_t pcg =
-      sizeof(T) * (static_cast<size_t>(K) * (NB * NB + fused_ls(NB)) + 3 * K * NB + 64);
-  const size_t form = sizeof(T) * static_cast<size_t>(FL::total(K));
-  return std::max(pcg, form);
+  return sizeof(T) * FL::elems(FL::kcap(K <= kHalfWarps ? 1 : 2));
 }
 
 // (n, m) -> the compiled shape: (14, 7) exactly (the BASELINE iiwa shape),
@@ -1090,11 +1111,7 @@ bool fused_supported(int K, int n, int m, int kind) {
   return with_fused_shape(n, m, [&](auto nb, auto mb, auto) {
     constexpr int NB = decltype(nb)::value, MB = decltype(mb)::value;
     using FL = FLayout<T, NB, MB>;
-    // the theta^-1 pass's group tiles (groups < K + 3) stay clear of the theta
-    // rows F2 leaves at the end of the tile region
-    // (and of the D blocks left in place, oD)
-    const bool tiles_ok = (K + 3) * FL::g8_tile <= FL::oD(K);
-    return tiles_ok && fused_smem_bytes<T, NB, MB>(K) + 64 <= 227 * 1024;
+    return K <= FL::kcap(K <= kHalfWarps ? 1 : 2);
   });
 }
 
