@@ -402,10 +402,57 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
     {
       constexpr bool PADQ = NB < 16, PADR = MB < 8;
       const int w = tid >> 5, fr = lane >> 2, fc = lane & 3;
+      // global operand fragments of row bb (A, B from L2, R_k^-1 from the
+      // slot, e_k), fetched one row ahead: their L2 latency overlaps the
+      // previous row's tensor-core chains. A (row r, col c), B (row c, col r).
+      auto fetch = [&](int bb, T (&af)[2][4], T (&bf)[2][2], T (&rf)[2], T (&ek)[2]) {
+        const bool lv = bb >= 1 && bb < K;
+        const int k = lv ? bb - 1 : 0;
+        const T* Ak = As + static_cast<size_t>(k) * nn;
+        const T* Bk = Bs + static_cast<size_t>(k) * nm;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int i = mt * 8 + fr;
+          // e_k rows for gamma (lane (r, 0) owns rows r and r + 8)
+          ek[mt] = (lv && fc == 0 && i < NB) ? __ldg(es + k * NB + i) : T(0);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const int q = ks * 4 + fc;
+            af[mt][ks] = (lv && i < NB && q < NB) ? __ldg(Ak + i * NB + q) : T(0);
+          }
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int q = ks * 4 + fc;
+            bf[mt][ks] = (lv && i < NB && q < m && (EXM || q < MB)) ? __ldg(Bk + i * m + q) : T(0);
+          }
+        }
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int sr = ks * 4 + fc;
+          T v = T(0);
+          if (lv && sr < MB)
+            v = fr < MB ? __ldcg(gR + static_cast<size_t>(k) * mm + sr * MB + fr)
+                        : ((PADR && fr == MB) ? srr[k * 8 + sr] : T(0));
+          rf[ks] = v;
+        }
+      };
+      T afn[2][4], bfn[2][2], rfn[2], ekn[2];
+      fetch(w, afn, bfn, rfn, ekn);
 #pragma unroll 1
       for (int t = 0; t < 4; ++t) {
         const int b = w + 16 * t;
         const bool live = b >= 1 && b < K;  // warp-uniform
+        T af[2][4], bf[2][2], rf[2], ek[2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          ek[mt] = ekn[mt];
+          rf[mt] = rfn[mt];
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) af[mt][ks] = afn[mt][ks];
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) bf[mt][ks] = bfn[mt][ks];
+        }
+        if (t < 3) fetch(b + 16, afn, bfn, rfn, ekn);
         if (b == 0) {
           // schur.cpp:53-57: S(0,0) = D_0 = Q_0^-1, theta_inv[0] = sym(Q_0), gamma_0
           if (lane < NB) {
@@ -430,49 +477,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
           const T* Bk = Bs + static_cast<size_t>(k) * nm;
           const T* Xk = sQi + static_cast<size_t>(k) * NN;
           const T* Xk1 = Xk + NN;
-          // e_k rows for gamma, issued first (their latency hides behind the
-          // tensor-core chains; lane (r, 0) owns rows r and r + 8)
-          T ek[2];
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            const int i = mt * 8 + fr;
-            ek[mt] = (fc == 0 && i < NB) ? __ldg(es + k * NB + i) : T(0);
-          }
-          // operand fragments: A (row r, col c), B (row c, col r)
-          T af[2][4], bf[2][2], xf[2][4], rf[2];
-#pragma unroll
-          for (int mt = 0; mt < 2; ++mt) {
-            const int i = mt * 8 + fr;
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              const int q = ks * 4 + fc;
-              af[mt][ks] = (i < NB && q < NB) ? __ldg(Ak + i * NB + q) : T(0);
-            }
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
-              const int q = ks * 4 + fc;
-              bf[mt][ks] = (i < NB && q < m && (EXM || q < MB)) ? __ldg(Bk + i * m + q) : T(0);
-            }
-          }
+          // Q_k^-1 fragments (B operand, row q, col j) from shared memory; pad
+          // column NB carries Q_k^-1 q_k (one predicated load, no branches)
+          T xf[2][4];
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
             const int j = nt * 8 + fr;
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks) {
               const int q = ks * 4 + fc;
-              T v = T(0);
-              if (q < NB) v = j < NB ? Xk[q * NB + j] : ((PADQ && j == NB) ? sqq[k * 16 + q] : T(0));
-              xf[nt][ks] = v;
+              const T* src = j < NB ? Xk + q * NB + j : sqq + k * 16 + q;
+              const bool ok = q < NB && (j < NB || (PADQ && j == NB));
+              xf[nt][ks] = ok ? *src : T(0);
             }
-          }
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const int sr = ks * 4 + fc;
-            T v = T(0);
-            if (sr < MB)
-              v = fr < MB ? __ldcg(gR + static_cast<size_t>(k) * mm + sr * MB + fr)
-                          : ((PADR && fr == MB) ? srr[k * 8 + sr] : T(0));
-            rf[ks] = v;
           }
           // AQ (16 DMMA)
           T aq[2][2][2];

@@ -133,7 +133,10 @@ __device__ __forceinline__ void dot2_chunks(unsigned t0, unsigned t1, const doub
     unsigned u[2 * C], w[2 * C];
     ld_words<2 * C>(t0 + 2 * J0, u);
     ld_words<2 * C>(t1 + 2 * J0, w);
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+    // no "memory" clobber: TMEM is not compiler-visible memory, so the shared
+    // loads of x are free to be scheduled across the wait (they overlap the
+    // TMEM latency instead of starting after it)
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
 #pragma unroll
     for (int i = 0; i < 2 * C; ++i) asm volatile("" : "+r"(u[i]), "+r"(w[i]));
 #pragma unroll

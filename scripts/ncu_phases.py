@@ -72,23 +72,34 @@ def main(csv_path, sass_path, kernel="_ZN3b2p11k_fused_ctaIdLi14ELi7ELi2ELb1ELb0
             return float(r[hdr[k]].replace(",", ""))
         except (ValueError, KeyError):
             return 0.0
+    reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
     acc = defaultdict(lambda: [0.0, 0.0, 0.0])
+    why = defaultdict(lambda: defaultdict(float))
+    last = "prologue"  # rematerialised prologue values count to the enclosing phase
     for r in rows:
         ln = lm.get(int(r[0], 16) - base)
-        ph = "prologue"
-        if ln is not None:
+        ph = last
+        if ln is not None and ln >= starts[0][0]:
+            ph = "prologue"
             for s, name in starts:
                 if ln >= s:
                     ph = name
+            last = ph
         a = acc[ph]
         a[0] += f(r, "Warp Stall Sampling (All Samples)")
         a[1] += f(r, "L1 Wavefronts Shared")
         a[2] += f(r, "Instructions Executed")
+        for h in reasons:
+            why[ph][h] += f(r, h)
     tot = [sum(a[i] for a in acc.values()) or 1 for i in range(3)]
     print(f"phase starts (line): {starts}")
     for ph, a in sorted(acc.items(), key=lambda kv: -kv[1][0]):
         print(f"{ph:>10}: samples {100 * a[0] / tot[0]:5.1f}%  shared wavefronts {100 * a[1] / tot[1]:5.1f}%"
               f"  warp instructions {100 * a[2] / tot[2]:5.1f}%")
+        w = why[ph]
+        tw = sum(w.values()) or 1
+        top = sorted(w.items(), key=lambda kv: -kv[1])[:6]
+        print("            stalls: " + ", ".join(f"{k[6:]} {100 * v / tw:.0f}%" for k, v in top))
 
 
 if __name__ == "__main__":
