@@ -318,6 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
         for (int i = 0; i < MB; ++i)  // identity pad rows / columns past m
           ra[i] = (EXM || (lm < m && i < m)) ? __ldg(Rr + i) : (lm == i ? T(1) : T(0));
       }
+      // r_g[gl] (for R_g^-1 r_g after the inverse; shuffled to the group then)
+      const T rl = (gl < MB && (EXM || gl < m)) ? __ldg(rs + static_cast<size_t>(rc) * m + gl) : T(0);
       T a0[NB], a1[NB], x0[NB], x1[NB];
       // clamped duplicates read Q_{K-1} from global memory (its shared copy
       // is inverted in place by its owner)
@@ -370,12 +372,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
       T xr[MB];
       const int fr = g8_spd_inverse<T, MB>(ra, gt, gt + MB * MB, gt + FL::g8_tile - 16, gl, xr);
       if (rv && fr >= 0) fkey = min(fkey, 4 * (g + 1) + 1);
+      T rsv[MB];
+#pragma unroll
+      for (int i = 0; i < MB; ++i) rsv[i] = __shfl_sync(FULL, rl, i, 8);
       if (rv && gl < MB) {
         T rr = T(0);
 #pragma unroll
         for (int i = 0; i < MB; ++i) {
           gR[static_cast<size_t>(g) * mm + i * MB + gl] = xr[i];
-          rr += xr[i] * ((EXM || i < m) ? rs[g * m + i] : T(0));
+          rr += xr[i] * rsv[i];
         }
         srr[g * 8 + gl] = rr;
       }

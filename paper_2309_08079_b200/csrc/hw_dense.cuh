@@ -359,19 +359,23 @@ __device__ __forceinline__ int g8x2_spd_inverse(T (&a0)[N], T (&a1)[N], T* Lr, T
     fail = (bad && fail < 0) ? k : fail;
     piv = bad ? T(1) : piv;
     const T r = rsqrt(piv);
+    // The stores below are unconditional (no divergent branches): a lane
+    // whose row is above the pivot writes its partial into the upper triangle
+    // of Lr, which is never read; the duplicate lanes (l >= H) store exactly
+    // lane H - 1's values; rd[k] is group-uniform.
     if (k < H) {
       const T v0 = (lr == k ? piv : s0) * r;
       const bool own0 = act && lr >= k;
       a0[k] = own0 ? v0 : a0[k];
-      if (own0) Lr[lr * N + k] = v0;
+      Lr[lr * N + k] = v0;
     }
     {
       const T v1 = (lr + H == k ? piv : s1) * r;
       const bool own1 = act && lr + H >= k;
       a1[k] = own1 ? v1 : a1[k];
-      if (own1) Lr[(lr + H) * N + k] = v1;
+      Lr[(lr + H) * N + k] = v1;
     }
-    if (act && lr == (k < H ? k : k - H)) rd[k] = r;
+    rd[k] = r;
     __syncwarp();
   }
   // columns l and l + H of L^-1
@@ -390,12 +394,10 @@ __device__ __forceinline__ int g8x2_spd_inverse(T (&a0)[N], T (&a1)[N], T* Lr, T
     y1[i] = t1 * d;
   }
   __syncwarp();  // LiT may alias Lr
-  if (act) {
 #pragma unroll
-    for (int q = 0; q < N; q += 2) {
-      *reinterpret_cast<double2*>(LiT + lr * N + q) = make_double2(y0[q], y0[q + 1]);
-      *reinterpret_cast<double2*>(LiT + (lr + H) * N + q) = make_double2(y1[q], y1[q + 1]);
-    }
+  for (int q = 0; q < N; q += 2) {  // (duplicate lanes store lane H - 1's rows)
+    *reinterpret_cast<double2*>(LiT + lr * N + q) = make_double2(y0[q], y0[q + 1]);
+    *reinterpret_cast<double2*>(LiT + (lr + H) * N + q) = make_double2(y1[q], y1[q + 1]);
   }
   __syncwarp();
   // X[i][c] = sum_{q >= i} LiT[i][q] y_c[q]; y_c[i] dies with row i
