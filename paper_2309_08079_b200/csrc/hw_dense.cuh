@@ -440,7 +440,7 @@ __device__ __forceinline__ int g8_spd_inverse(T (&a)[N], T* Lr, T* LiT, T* rd, i
     const bool own = l >= k && l < N;
     a[k] = own ? val : a[k];
     if (own) Lr[l * N + k] = val;
-    if (l == k) rd[k] = r;
+    rd[k] = r;  // group-uniform (piv is the pivot lane's): no divergent store
     __syncwarp();
   }
   T y[N];
