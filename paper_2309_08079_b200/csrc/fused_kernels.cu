@@ -208,6 +208,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   T* st = sp + KL * NB;
   T* su = st + KL * NB;
   T* red = su + KL * NB;                        // [32]
+  // F2 leaves gamma_b in su (read once by the PCG stage, before the first
+  // preconditioner application writes u) where u clears Q_k^-1 q_k / R_k^-1
+  // r_k, which F2 reads, and the theta^-1 pass's group tiles (the c4 layout);
+  // otherwise in the global slot
+  constexpr bool kGamS = FL::osp(KL) + 2 * KL * NB >= FL::orr(KL) + (KL - 1) * 8 &&
+                         FL::osp(KL) + 2 * KL * NB >= (KL + 3) * FL::g8_tile;
   // D_b rows stay where the formation left them: theta_b (b >= 1) at the end
   // of the tile region (F2), D_0 = Q_0^-1 just before (FLayout::oD)
   T* sD = smem + FL::oD(KL);                    // [K][NB][NB]  D row products
@@ -248,8 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
   T* gL = p.slot + static_cast<size_t>(blockIdx.x) * fused_slot_stride<T>(K, NB, MB, keep_q);
   T* gD = gL + static_cast<size_t>(K) * LS;
   T* gT = gD + static_cast<size_t>(K) * NN;
-  T* gG = gT + static_cast<size_t>(K) * NN;  // gamma [K][NB]
-  T* gR = gG + static_cast<size_t>(K) * NB;  // R_k^-1 [N][MB][MB]
+  T* gG = kGamS ? su : gT + static_cast<size_t>(K) * NN;  // gamma [K][NB]
+  T* gR = gT + static_cast<size_t>(K) * (NN + NB);  // R_k^-1 [N][MB][MB]
   T* gQ = gR + static_cast<size_t>(K) * MB * MB;  // Q_k^-1 [K][NB][NB] (fused finish only)
 
   for (int sys = blockIdx.x; sys < p.B; sys += gridDim.x) {
@@ -762,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_cta(FusedParams<T> p) {
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int row = pr + H * c;
-      gam[c] = __ldcg(gG + pbc * NB + row);
+      gam[c] = kGamS ? gG[pbc * NB + row] : __ldcg(gG + pbc * NB + row);
       lam[c] = (pact && p.lambda0) ? p.lambda0[static_cast<size_t>(sys) * K * NB + pbc * NB + row]
                                    : T(0);
     }

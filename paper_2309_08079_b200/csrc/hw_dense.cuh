@@ -12,6 +12,28 @@ namespace hwd {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Predicated shared-memory stores (@p st.shared): the inverse routines' "only
+// the owning lane stores" steps without the divergent branches the compiler
+// otherwise builds around them.
+__device__ __forceinline__ void sts_if(double* a, double v, bool pred) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.shared.f64 [%0], %1;\n}\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(a))),
+               "d"(v), "r"(static_cast<unsigned>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void sts_if(float* a, float v, bool pred) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q st.shared.f32 [%0], %1;\n}\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(a))),
+               "f"(v), "r"(static_cast<unsigned>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void sts2_if(double* a, double v0, double v1, bool pred) {
+  asm volatile("{\n.reg .pred q;\nsetp.ne.u32 q, %3, 0;\n@q st.shared.v2.f64 [%0], {%1, %2};\n}\n" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(a))),
+               "d"(v0), "d"(v1), "r"(static_cast<unsigned>(pred))
+               : "memory");
+}
+
 template <int N>
 struct Odd {
   static constexpr int v = N | 1;
@@ -359,23 +381,20 @@ __device__ __forceinline__ int g8x2_spd_inverse(T (&a0)[N], T (&a1)[N], T* Lr, T
     fail = (bad && fail < 0) ? k : fail;
     piv = bad ? T(1) : piv;
     const T r = rsqrt(piv);
-    // The stores below are unconditional (no divergent branches): a lane
-    // whose row is above the pivot writes its partial into the upper triangle
-    // of Lr, which is never read; the duplicate lanes (l >= H) store exactly
-    // lane H - 1's values; rd[k] is group-uniform.
+    // predicated stores (sts_if): no divergent branches around them
     if (k < H) {
       const T v0 = (lr == k ? piv : s0) * r;
       const bool own0 = act && lr >= k;
       a0[k] = own0 ? v0 : a0[k];
-      Lr[lr * N + k] = v0;
+      sts_if(Lr + lr * N + k, v0, own0);
     }
     {
       const T v1 = (lr + H == k ? piv : s1) * r;
       const bool own1 = act && lr + H >= k;
       a1[k] = own1 ? v1 : a1[k];
-      Lr[(lr + H) * N + k] = v1;
+      sts_if(Lr + (lr + H) * N + k, v1, own1);
     }
-    rd[k] = r;
+    sts_if(rd + k, r, act && lr == (k < H ? k : k - H));
     __syncwarp();
   }
   // columns l and l + H of L^-1
@@ -395,9 +414,9 @@ __device__ __forceinline__ int g8x2_spd_inverse(T (&a0)[N], T (&a1)[N], T* Lr, T
   }
   __syncwarp();  // LiT may alias Lr
 #pragma unroll
-  for (int q = 0; q < N; q += 2) {  // (duplicate lanes store lane H - 1's rows)
-    *reinterpret_cast<double2*>(LiT + lr * N + q) = make_double2(y0[q], y0[q + 1]);
-    *reinterpret_cast<double2*>(LiT + (lr + H) * N + q) = make_double2(y1[q], y1[q + 1]);
+  for (int q = 0; q < N; q += 2) {
+    sts2_if(LiT + lr * N + q, y0[q], y0[q + 1], act);
+    sts2_if(LiT + (lr + H) * N + q, y1[q], y1[q + 1], act);
   }
   __syncwarp();
   // X[i][c] = sum_{q >= i} LiT[i][q] y_c[q]; y_c[i] dies with row i
@@ -439,8 +458,8 @@ __device__ __forceinline__ int g8_spd_inverse(T (&a)[N], T* Lr, T* LiT, T* rd, i
     const T val = (l == k ? piv : s) * r;
     const bool own = l >= k && l < N;
     a[k] = own ? val : a[k];
-    if (own) Lr[l * N + k] = val;
-    rd[k] = r;  // group-uniform (piv is the pivot lane's): no divergent store
+    sts_if(Lr + l * N + k, val, own);
+    sts_if(rd + k, r, l == k);
     __syncwarp();
   }
   T y[N];
