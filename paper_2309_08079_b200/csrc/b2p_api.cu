@@ -523,7 +523,21 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     const int g = env_int("B2P_FC_G", 0);
     if ((K + g - 1) / g <= 32 && (K + ((K + g - 1) / g) - 1) / ((K + g - 1) / g) == g) fcG = g;
   }
-  const bool one_cta_ok = fused_supported<T>(K, n, k->m, kind);
+  // n = 7, 8 (n = 7 through the identity pad): the one-CTA kernel when the
+  // small-block kernel does not cover the shape, and for horizons K > 24
+  // (batches; single solves only at n = 8, where no pad copies are needed).
+  // Measured (scripts/onecta_small_probe.py, profiles/r02_onecta_small.json):
+  // 4096 x K 64: n7 m2 1.65 -> 2.49 M/s, n8 m4 1.58 -> 2.96 M/s; K 17: small-block
+  // 3.9 vs 3.8 M/s; K 9: 8.7 vs 4.1 M/s. B2P_ONECTA_MIN_N=<n> overrides (n >= it).
+  const int onecta_floor = env_int("B2P_ONECTA_MIN_N", -1);
+  auto onecta_n = [&](int nn) -> bool {
+    if (onecta_floor >= 0) return nn >= onecta_floor;
+    if (nn >= 9) return true;
+    if (nn < 7) return false;
+    const bool small_ok = env_int("B2P_SMALL", 1) && small_supported<T>(K, nn, k->m, kind);
+    return !small_ok || (K > 24 && (B > 1 || nn == 8));
+  };
+  const bool one_cta_ok = onecta_n(n) && fused_supported<T>(K, n, k->m, kind);
   // Fused grid kernel: one long-horizon system over G co-resident CTAs (the
   // default for shapes no cluster / one-CTA kernel covers, e.g. c5);
   // B2P_FG=1 forces it, =0 disables it; B2P_FG_RP picks the rows per CTA.
@@ -674,12 +688,12 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     if (time_it) CK(cudaEventRecord(c->ev1, st));
     return false;
   }
-  // Odd n in [9, 15] on the one-CTA kernel: the state dimension padded to n + 1
+  // Odd n in [7, 15] on the one-CTA kernel: the state dimension padded to n + 1
   // (Q with an identity pad, A / B / q / e / x pads zero). Every pad entry of
   // S, gamma, theta^-1 and of every PCG vector is then exactly zero, so the
   // real rows follow the unpadded recurrence (the dot products only gain
   // exact zero terms); lambda is cropped back.
-  const bool pad_ok = !drift && !dz_dev && sizeof(T) == 8 && (n & 1) && n >= 9 && n + 1 <= 16 &&
+  const bool pad_ok = !drift && !dz_dev && sizeof(T) == 8 && (n & 1) && onecta_n(n) && n + 1 <= 16 &&
                       env_int("B2P_FUSED", 1) && env_int("B2P_PAD", 1) &&
                       fused_supported<T>(K, n + 1, k->m, kind);
   if (pad_ok) {
@@ -753,7 +767,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     if (time_it) CK(cudaEventRecord(c->ev1, st));
     return false;
   }
-  if (!drift && env_int("B2P_FUSED", 1) && fused_supported<T>(K, n, k->m, kind)) {
+  if (!drift && env_int("B2P_FUSED", 1) && one_cta_ok) {
     // persistent one-CTA-per-system K1+K3 kernel (fused_kernels.cu)
     const int grid = std::max(1, std::min(B, c->sm_count));
     FusedParams<T> f{};

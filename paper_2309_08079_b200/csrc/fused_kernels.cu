@@ -1111,7 +1111,7 @@ size_t fused_smem_bytes(int K) {  // the layout of the instantiation K launches
 }
 
 // (n, m) -> the compiled shape: (14, 7) exactly (the BASELINE iiwa shape),
-// else even n in [10, 16] with m <= 8 padded to MB = 4 or 8 (runtime m).
+// else even n in [8, 16] with m <= 8 padded to MB = 4 or 8 (runtime m).
 template <class F>
 bool with_fused_shape(int n, int m, F&& f) {
   using std::integral_constant;
@@ -1119,6 +1119,8 @@ bool with_fused_shape(int n, int m, F&& f) {
   if (m < 1 || m > 8) return false;
   const bool m4 = m <= 4;
   switch (n) {
+    case 8: return m4 ? f(integral_constant<int, 8>{}, integral_constant<int, 4>{}, std::false_type{})
+                      : f(integral_constant<int, 8>{}, integral_constant<int, 8>{}, std::false_type{});
     case 10: return m4 ? f(integral_constant<int, 10>{}, integral_constant<int, 4>{}, std::false_type{})
                        : f(integral_constant<int, 10>{}, integral_constant<int, 8>{}, std::false_type{});
     case 12: return m4 ? f(integral_constant<int, 12>{}, integral_constant<int, 4>{}, std::false_type{})

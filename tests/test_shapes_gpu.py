@@ -1,5 +1,5 @@
 """Off-BASELINE shapes on the fused one-CTA kernel (k_fused_cta templated over
-even n in [10, 16] and m <= 8, the control dimension padded to 4 / 8 with
+even n in [8, 16] and m <= 8, the control dimension padded to 4 / 8 with
 identity R and zero B, r pads): per-system parity with the oracle (identical
 PCG iteration counts, lambda within 1e-10), every preconditioner kind, ragged
 horizons, warm start / cap / non-PD messages, build_schur's formation-only
@@ -144,4 +144,63 @@ def test_odd_n_padded_single_warm_start_cap_and_errors(api, orc):
     bad = orc.random_kkt(8702, 47, 13, 5)
     bad.Q[5] = -np.eye(13)
     with pytest.raises(RuntimeError, match="build_schur: Q at knot 5 is not positive definite"):
+        api.solve(bad, PrecondKind.symmetric_stair, cfg=cfg)
+
+
+SMALL_N = [(64, 8, 4), (64, 7, 2), (64, 8, 8), (48, 7, 7), (33, 8, 1)]
+
+
+@pytest.mark.parametrize("K,n,m", SMALL_N)
+def test_small_n_long_horizon_batches_on_one_cta(api, orc, env, K, n, m):
+    """n = 7, 8 at horizons K > 24: the one-CTA kernel (n = 7 through the
+    identity pad to 8) instead of the small-block kernel; every stair-family
+    kind against the oracle per system."""
+    env["B2P_FC"] = "0"
+    B = 20
+    kb = api.random_kkt_batch(8800 + 5 * n + m + K, B, K - 1, n, m)
+    cfg = PcgConfig(epsilon=1e-8)
+    for kind in (PrecondKind.symmetric_stair, PrecondKind.stair, PrecondKind.block_jacobi):
+        lam, reps = api.solve_batched(kb, kind, 1, cfg)
+        assert api.context().last_path() == 1  # the one-CTA fused kernel
+        _, lo, ro = orc.solve_batch(kb, kind, 1, cfg)
+        assert np.array_equal(reps.iterations, np.array([r.iterations for r in ro]))
+        assert np.array_equal(reps.converged, np.array([bool(r.converged) for r in ro]))
+        scale = np.maximum(1.0, np.abs(lo).max(axis=1))
+        assert (np.abs(lam - lo).max(axis=1) / scale).max() <= TOL64
+
+
+def test_small_n_policy_and_n8_single_solve_finish(api, orc, env):
+    """Short horizons stay on the small-block kernel; n = 8 single solves at
+    K 64 take the one-CTA kernel, with warm start, cap, the fused sqp_step
+    finish and the non-PD message; B2P_ONECTA_MIN_N overrides the policy."""
+    env["B2P_FC"] = "0"
+    kb = api.random_kkt_batch(8901, 8, 16, 8, 4)  # K 17
+    api.solve_batched(kb, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
+    assert api.context().last_path() != 1
+    env["B2P_ONECTA_MIN_N"] = "7"
+    lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
+    assert api.context().last_path() == 1
+    _, lo, ro = orc.solve_batch(kb, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
+    assert np.array_equal(reps.iterations, np.array([r.iterations for r in ro]))
+    del env["B2P_ONECTA_MIN_N"]
+    kkt = orc.random_kkt(8902, 63, 8, 4)
+    cfg = PcgConfig(epsilon=1e-8)
+    got = api.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    assert api.context().last_path() == 1
+    want = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
+    assert got.report.iterations == want.report.iterations
+    assert rel_inf_error(got.lambda_, want.lambda_) <= TOL64
+    warm = api.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg, lambda0=0.5 * want.lambda_)
+    ow = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg, lambda0=0.5 * want.lambda_)
+    assert warm.report.iterations == ow.report.iterations
+    capped = api.solve(kkt, PrecondKind.symmetric_stair, cfg=PcgConfig(epsilon=1e-14, max_iter=3))
+    oc = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=PcgConfig(epsilon=1e-14, max_iter=3))
+    assert not capped.report.converged and capped.report.iterations == 3
+    assert rel_inf_error(capped.lambda_, oc.lambda_) <= TOL64
+    res, dz = api.sqp_step(kkt, cfg=cfg)
+    odz = orc.reconstruct_primal(kkt, want.lambda_)
+    assert np.abs(dz - odz).max() / max(1.0, np.abs(odz).max()) <= 1e-9
+    bad = orc.random_kkt(8903, 63, 8, 4)
+    bad.Q[9] = -np.eye(8)
+    with pytest.raises(RuntimeError, match="build_schur: Q at knot 9 is not positive definite"):
         api.solve(bad, PrecondKind.symmetric_stair, cfg=cfg)
