@@ -66,3 +66,13 @@ dz = torch.empty((7, kb.primal_dim()), dtype=torch.float64, device="cuda")
 api.reconstruct_primal_batched_device(kd, lamd.data_ptr(), dz.data_ptr(), 7)
 torch.cuda.synchronize()
 print("streaming reconstruct_primal", float(dz.abs().sum()))
+# n = 7, 8 on the one-CTA kernel (NB = 8 instantiation; n = 7 through the pad)
+kb = api.random_kkt_batch(17, 6, 39, 8, 4)
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("batched one-CTA n8", api.context().last_path(), [x.iterations for x in reps])
+kb = api.random_kkt_batch(18, 6, 39, 7, 2)
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("batched one-CTA n7 padded", api.context().last_path(), [x.iterations for x in reps])
+k8 = api.random_kkt(19, 39, 8, 4)
+res, dz8 = api.sqp_step(k8, cfg=cfg)
+print("one-CTA n8 sqp_step", api.context().last_path(), res.report.iterations)
