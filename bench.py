@@ -661,12 +661,16 @@ def run_b200(a, world, rank, local):
         ev_ms = allmax(ev_ms)
         assert np.array_equal(lam_host, lam_host_dev), "e2e/device outputs differ"
         sysout = 56  # sizeof(SysOut) copied back per system
+        h2d = ctx_h.last_h2d_bytes()  # what the call moved (Q_k / R_k as lower triangles)
         e2e = {"value": world * B * a.steps / wall_s, "unit": UNIT,
-               "h2d_bytes_per_step": B * kkt_bytes(N, n, m),
+               "h2d_bytes_per_step": h2d,
+               "h2d_bytes_full_blocks": B * kkt_bytes(N, n, m),
                "d2h_bytes_per_step": B * (D * 8 + sysout + 4),
                "timing": "host wall clock around b2p_solve_batched",
                "value_cuda_events": world * B * a.steps / (ev_ms * 1e-3),
-               "path": "b2p_solve_batched (host pinned buffers, 2-stream chunked H2D/compute/D2H)"}
+               "path": "b2p_solve_batched (host pinned buffers, 2-stream chunked H2D/compute/D2H; "
+                       "Q_k and R_k sent as lower triangles and mirrored on the device — the "
+                       "reference's LLT / LDLT read only the lower triangle, schur.cpp:16)"}
         ctx_h.close()
 
     # ---- every other BASELINE row (rank 0)

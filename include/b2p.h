@@ -256,6 +256,10 @@ int b2p_direct_solve_batched_device(b2p_ctx* ctx, int dtype, int batch, const b2
 
 /* Device time (ms) of the most recent solve kernels on this context. */
 int b2p_ctx_last_solve_ms(b2p_ctx* ctx, float* ms);
+/* Host -> device bytes moved by the most recent b2p_solve_batched on this
+ * context (Q_k / R_k travel as lower triangles, mirrored on the device: the
+ * reference's LLT / LDLT read only the lower triangle, schur.cpp:16). */
+int b2p_ctx_last_h2d_bytes(b2p_ctx* ctx, unsigned long long* bytes);
 /* Per-kernel split of the most recent fused solve: ms[0] = K1 Schur
  * formation, ms[1] = K3 PCG (CUDA events on the launch stream; n >= 2).
  * Valid after the caller synchronised the stream. */

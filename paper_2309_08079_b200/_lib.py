@@ -41,6 +41,7 @@ def load() -> C.CDLL:
         "b2p_ctx_last_path": ([vp], i32),
         "b2p_ctx_phase_stamps": ([vp, vp, i32], i32),
         "b2p_ctx_last_solve_ms": ([vp, C.POINTER(C.c_float)], i32),
+        "b2p_ctx_last_h2d_bytes": ([vp, C.POINTER(C.c_ulonglong)], i32),
         "b2p_ctx_last_phase_ms": ([vp, C.POINTER(C.c_float), i32], i32),
         "b2p_ctx_phase_accounting": ([vp, i32], i32),
         "b2p_ctx_phase_totals": ([vp, C.POINTER(C.c_float), i32, C.POINTER(i32)], i32),
@@ -85,6 +86,7 @@ EXPORTED = [
     "b2p_ctx_set_stream", "b2p_ctx_stream", "b2p_ctx_kernel_launches", "b2p_ctx_last_path",
     "b2p_ctx_phase_stamps",
     "b2p_ctx_last_solve_ms",
+    "b2p_ctx_last_h2d_bytes",
     "b2p_ctx_last_phase_ms", "b2p_ctx_phase_accounting", "b2p_ctx_phase_totals",
     "b2p_blocktri_matvec", "b2p_blocktri_cholesky_solve", "b2p_blocktri_check",
     "b2p_build_schur", "b2p_stair_matrix", "b2p_build_preconditioner",

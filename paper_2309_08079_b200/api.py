@@ -51,6 +51,13 @@ class Context:
         self._lib.b2p_ctx_last_solve_ms(self.handle, C.byref(v))
         return float(v.value)
 
+    def last_h2d_bytes(self) -> int:
+        """Host -> device bytes of the most recent solve_batched call (Q_k / R_k
+        travel as lower triangles)."""
+        v = C.c_ulonglong()
+        self._lib.b2p_ctx_last_h2d_bytes(self.handle, C.byref(v))
+        return int(v.value)
+
     def last_phase_ms(self) -> tuple[float, float]:
         """(K1 formation ms, K3 PCG ms) of the most recent fused solve."""
         v = (C.c_float * 2)()

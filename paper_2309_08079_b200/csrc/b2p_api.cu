@@ -3,6 +3,7 @@
 // batched / multi-GPU drivers. No CPU fallback: every compute entry point
 // runs on the device or fails with B2P_CUDA_ERROR.
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <atomic>
@@ -13,7 +14,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <random>
 #include <string>
@@ -24,6 +27,67 @@
 #include "kernels.h"
 
 using namespace b2p;
+
+// Persistent host worker pool (the packed batch upload): run(n, f) splits
+// [0, n) over the workers and the calling thread and returns when all ranges
+// are done.
+struct HostPool {
+  std::vector<std::thread> th;
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::function<void(size_t, size_t)> fn;
+  size_t n = 0;
+  int T = 1, pending = 0;
+  unsigned long long gen = 0;
+  bool stop = false;
+  explicit HostPool(int t) : T(t < 1 ? 1 : t) {
+    for (int i = 1; i < T; ++i) th.emplace_back([this, i] { loop(i); });
+  }
+  void loop(int i) {
+    unsigned long long seen = 0;
+    for (;;) {
+      std::function<void(size_t, size_t)> f;
+      size_t nn;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+        f = fn;
+        nn = n;
+      }
+      f(nn * i / T, nn * (i + 1) / T);
+      std::lock_guard<std::mutex> lk(mu);
+      if (--pending == 0) done_cv.notify_one();
+    }
+  }
+  template <class F>
+  void run(size_t n_, F&& f) {
+    if (T == 1 || n_ < 64) {
+      f(size_t(0), n_);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      fn = f;
+      n = n_;
+      pending = T - 1;
+      ++gen;
+    }
+    cv.notify_all();
+    f(size_t(0), n_ / T);
+    std::unique_lock<std::mutex> lk(mu);
+    done_cv.wait(lk, [&] { return pending == 0; });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+  }
+};
 
 struct b2p_ctx {
   int device = 0;
@@ -39,6 +103,7 @@ struct b2p_ctx {
   std::vector<cudaEvent_t> pool;
   size_t pool_used = 0;
   float last_ms = 0.f;
+  size_t last_h2d_bytes = 0;  // host -> device bytes of the last b2p_solve_batched
   // next LL epoch of the fused grid kernel, one counter per LL buffer (tag):
   // a buffer's words are only ever compared against its own epochs
   std::map<std::string, unsigned> fg_epoch;
@@ -48,6 +113,7 @@ struct b2p_ctx {
   std::atomic<long long> launches{0};
   int sm_count = 148;
   size_t smem_optin = 227 * 1024;
+  std::unique_ptr<HostPool> host_pool;  // created on first packed upload
   cudaStream_t stream() const { return user ? user : own; }
 };
 
@@ -504,6 +570,133 @@ void reblock(const void* in, void* out, long long nblocks, int ri, int ci, int r
   k_reblock<T><<<grid, 256, 0, st>>>(static_cast<const T*>(in), static_cast<T*>(out), nblocks, ri,
                                       ci, ro, co, diag);
   CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ packed upload
+// The solve path reads only the lower triangles of Q_k and R_k: every
+// factorisation is Eigen's LLT / LDLT, which reads the lower triangle
+// (schur.cpp:16, :61-63; kkt.cpp:171-177), and only theta_inv[0] = sym(Q_0)
+// (schur.cpp:56) reads an upper one. The host batch path therefore ships the
+// lower triangles (+ Q_0's strict upper triangle) over PCIe and mirrors them
+// on the device: 19 % fewer H2D bytes at c4, and any input — an asymmetric
+// Q_k or R_k included — is read exactly as the reference reads it.
+inline size_t tri(int n) { return static_cast<size_t>(n) * (n + 1) / 2; }
+
+// block b of `nblk` n x n blocks -> its lower triangle (row-major rows 0..r);
+// with k0 > 0, block s * k0 of every system s also gives its strict upper
+// triangle to `up` (row-major, row r: columns r+1..n-1)
+// 8-byte / 4-byte non-temporal stores: the staging is written once and read by
+// the DMA engine, so the stores bypass the cache (no read-for-ownership)
+inline void st_nt(double* p, double v) {
+  long long b;
+  std::memcpy(&b, &v, 8);
+  _mm_stream_si64(reinterpret_cast<long long*>(p), b);
+}
+inline void st_nt(float* p, float v) {
+  int b;
+  std::memcpy(&b, &v, 4);
+  _mm_stream_si32(reinterpret_cast<int*>(p), b);
+}
+template <class T>
+void pack_lower(const T* src, T* dst, T* up, int n, int k0, size_t b0, size_t b1) {
+  const size_t nn = static_cast<size_t>(n) * n, t = tri(n), tu = tri(n - 1);
+  for (size_t b = b0; b < b1; ++b) {
+    const T* a = src + b * nn;
+    T* o = dst + b * t;
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c <= r; ++c) st_nt(o++, a[r * n + c]);
+    if (k0 > 0 && b % k0 == 0) {
+      T* u = up + (b / k0) * tu;
+      for (int r = 0; r + 1 < n; ++r)
+        for (int c = r + 1; c < n; ++c) st_nt(u++, a[r * n + c]);
+    }
+  }
+  _mm_sfence();  // the streaming stores are visible before the DMA is issued
+}
+
+template <class T>
+__global__ void k_unpack_sym(const T* __restrict__ L, const T* __restrict__ U0, T* __restrict__ out,
+                             long long nblk, int n, int k0) {
+  const int nn = n * n, t = n * (n + 1) / 2, tu = n * (n - 1) / 2;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < nblk * nn;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long b = e / nn;
+    const int w = static_cast<int>(e - b * nn), r = w / n, c = w - r * n;
+    T v;
+    if (r >= c) {
+      v = L[b * t + r * (r + 1) / 2 + c];
+    } else if (k0 > 0 && b % k0 == 0) {
+      v = U0[(b / k0) * tu + r * (n - 1) - r * (r - 1) / 2 + (c - r - 1)];
+    } else {
+      v = L[b * t + c * (c + 1) / 2 + r];
+    }
+    out[e] = v;
+  }
+}
+template <class T>
+void unpack_sym(const void* L, const void* U0, void* out, long long nblk, int n, int k0,
+                cudaStream_t st) {
+  const long long total = nblk * n * n;
+  if (total <= 0) return;
+  const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 8192));
+  k_unpack_sym<T><<<grid, 256, 0, st>>>(static_cast<const T*>(L), static_cast<const T*>(U0),
+                                         static_cast<T*>(out), nblk, n, k0);
+  CK(cudaGetLastError());
+}
+
+// upload_kkt for the chunked batch pipeline with Q and R packed (see above):
+// the other arrays go straight from the caller's memory; Q / R are packed
+// into the pinned staging `hpk` (reused only after `ready`, the event of its
+// previous H2D) and mirrored on the device into the same layout upload_kkt
+// produces. Returns the H2D byte count through *h2d_bytes.
+template <class T>
+KktDev upload_kkt_packed(b2p_ctx* c, const b2p_kkt* k, int first, int count, void* dst,
+                         cudaStream_t st, const std::string& tag, cudaEvent_t ready,
+                         size_t* h2d_bytes) {
+  const size_t es = sizeof(T);
+  const size_t N = k->N, n = k->n, m = k->m, K = N + 1;
+  const size_t sz[9] = {K * n * n, K * n, N * m * m, N * m, N * n * n, N * n * m, N * n, n, n};
+  const void* src[9] = {k->Q, k->q, k->R, k->r, k->A, k->B, k->e, k->x_s, k->x0};
+  const void* out[9];
+  char* d = static_cast<char*>(dst);
+  size_t bytes_total = 0;
+  for (int a = 0; a < 9; ++a) {
+    const size_t bytes = sz[a] * es * count;
+    if (bytes && !src[a]) throw invalid("b2p_kkt: null array");
+    out[a] = d;
+    if (bytes && a != 0 && a != 2) {
+      h2d(c, d, static_cast<const char*>(src[a]) + sz[a] * es * first, bytes, st);
+      bytes_total += bytes;
+    }
+    d += (bytes + 255) / 256 * 256;
+  }
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  const size_t nq = K * count, nr = N * count;
+  const size_t bq = al(nq * tri(int(n)) * es), bu = al(count * tri(int(n) - 1) * es),
+               br = al(nr * tri(int(m)) * es);
+  char* h = static_cast<char*>(hws_get(c, tag + "pk", bq + bu + br));
+  char* dv = static_cast<char*>(ws_get(c, tag + "pkd", bq + bu + br));
+  CK(cudaEventSynchronize(ready));  // the staging's previous H2D has completed
+  const T* Qs = static_cast<const T*>(k->Q) + sz[0] * first;
+  const T* Rs = static_cast<const T*>(k->R) + (sz[2] ? sz[2] * first : 0);
+  T* hq = reinterpret_cast<T*>(h);
+  T* hu = reinterpret_cast<T*>(h + bq);
+  T* hr = reinterpret_cast<T*>(h + bq + bu);
+  if (!c->host_pool) {
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    c->host_pool.reset(new HostPool(std::min(hw, std::max(1, env_int("B2P_PACK_THREADS", 16)))));
+  }
+  c->host_pool->run(nq + nr, [&](size_t lo, size_t hi) {
+    if (lo < nq) pack_lower<T>(Qs, hq, hu, int(n), int(K), lo, std::min(hi, nq));
+    if (hi > nq && m > 0) pack_lower<T>(Rs, hr, nullptr, int(m), 0, std::max(lo, nq) - nq, hi - nq);
+  });
+  h2d(c, dv, h, bq + bu + br, st);
+  CK(cudaEventRecord(ready, st));
+  bytes_total += (nq * tri(int(n)) + count * tri(int(n) - 1) + nr * tri(int(m))) * es;
+  unpack_sym<T>(dv, dv + bq, const_cast<void*>(out[0]), static_cast<long long>(nq), int(n), int(K), st);
+  if (m > 0) unpack_sym<T>(dv + bq + bu, nullptr, const_cast<void*>(out[2]), static_cast<long long>(nr), int(m), 0, st);
+  if (h2d_bytes) *h2d_bytes += bytes_total;
+  return KktDev{out[0], out[1], out[2], out[3], out[4], out[5], out[6], out[7], out[8]};
 }
 
 template <class T>
@@ -1185,6 +1378,12 @@ int b2p_ctx_last_solve_ms(b2p_ctx* c, float* ms) {
   return B2P_OK;
 }
 
+int b2p_ctx_last_h2d_bytes(b2p_ctx* c, unsigned long long* bytes) {
+  if (!c || !bytes) return B2P_INVALID_ARGUMENT;
+  *bytes = static_cast<unsigned long long>(c->last_h2d_bytes);
+  return B2P_OK;
+}
+
 // ---------------------------------------------------------------- block_tri
 int b2p_blocktri_matvec(b2p_ctx* c, int dtype, int K, int nb, const void* M, const void* x,
                         int x_len, void* y, b2p_error* err) {
@@ -1786,6 +1985,15 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
     cudaEvent_t start = nullptr, stop = nullptr;
     CK(cudaEventCreate(&start));
     CK(cudaEventCreate(&stop));
+    // Q / R as packed lower triangles (upload_kkt_packed); B2P_PACK_SYM=0 sends
+    // the full blocks
+    const bool pack = env_int("B2P_PACK_SYM", 1) != 0 && n >= 2;
+    size_t h2d_total = 0;
+    cudaEvent_t ready[2] = {nullptr, nullptr};
+    for (auto& e : ready) {
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, streams[0]));
+    }
     CK(cudaEventRecord(start, streams[0]));
     CK(cudaStreamWaitEvent(streams[1], start, 0));
     for (int ci = 0; ci < nchunks; ++ci) {
@@ -1794,7 +2002,11 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
       cudaStream_t st = streams[sidx];
       const std::string tag = std::string("bh") + char('0' + sidx) + "_";
       void* in = ws_get(c, tag + "in", kkt_block_bytes(k, es, chunk));
-      const KktDev kv = upload_kkt(c, k, es, first, cnt, in, st, nullptr, 0, nullptr, false);
+      const KktDev kv =
+          !pack ? upload_kkt(c, k, es, first, cnt, in, st, nullptr, 0, nullptr, false)
+          : dtype == B2P_F64
+              ? upload_kkt_packed<double>(c, k, first, cnt, in, st, tag, ready[sidx], &h2d_total)
+              : upload_kkt_packed<float>(c, k, first, cnt, in, st, tag, ready[sidx], &h2d_total);
       char* dl0 = nullptr;
       if (lambda0) {
         dl0 = static_cast<char*>(ws_get(c, tag + "l0", es * D * chunk));
@@ -1824,6 +2036,13 @@ int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int ki
     cudaEventDestroy(start);
     cudaEventDestroy(stop);
     cudaEventDestroy(join);
+    for (auto& e : ready) cudaEventDestroy(e);
+    {
+      const size_t Nn = k->N, nn_ = k->n, mm_ = k->m, Kk = Nn + 1;
+      const size_t full = (Kk * nn_ * nn_ + Kk * nn_ + Nn * mm_ * mm_ + Nn * mm_ + Nn * nn_ * nn_ +
+                           Nn * nn_ * mm_ + Nn * nn_ + 2 * nn_) * es * batch;
+      c->last_h2d_bytes = (pack ? h2d_total : full) + (lambda0 ? es * D * batch : 0);
+    }
     if (!lam_pinned) std::memcpy(lambda_out, h_lam, es * D * batch);
     std::vector<SysOut> outs(h_outs, h_outs + batch);
     std::vector<int> keys(h_keys, h_keys + batch);

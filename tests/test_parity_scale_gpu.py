@@ -163,3 +163,56 @@ def test_chunked_pipeline_with_overlapping_chunks(api, env, kind):
         ctx.close()
         assert np.array_equal(lam1, lam2), chunk
         assert [r.iterations for r in rep1] == [r.iterations for r in rep2]
+
+
+@pytest.mark.parametrize("shape", [(63, 14, 7), (31, 12, 4), (20, 3, 2), (40, 13, 5)])
+def test_packed_upload_equals_full_blocks(api, env, shape):
+    """b2p_solve_batched ships Q_k / R_k as lower triangles (+ Q_0's upper
+    triangle) and mirrors them on the device: for symmetric inputs the results
+    equal the full-block upload bitwise, across many small chunks on two streams
+    (the packed staging is reused only after its previous H2D completed)."""
+    N, n, m = shape
+    B = 96
+    kb = api.random_kkt_batch(4242 + n, B, N, n, m)
+    cfg = PcgConfig(epsilon=1e-8)
+    env["B2P_PACK_SYM"] = "0"
+    ctx = api.Context(0)
+    lam0, rep0 = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg, ctx=ctx)
+    full = ctx.last_h2d_bytes()
+    ctx.close()
+    env["B2P_PACK_SYM"] = "1"
+    for chunk in ("512", "7"):
+        env["B2P_BATCH_CHUNK"] = chunk
+        ctx = api.Context(0)
+        lam1, rep1 = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg, ctx=ctx)
+        packed = ctx.last_h2d_bytes()
+        ctx.close()
+        assert np.array_equal(lam0, lam1), chunk
+        assert [r.iterations for r in rep0] == [r.iterations for r in rep1]
+        t = lambda d: d * (d + 1) // 2  # noqa: E731
+        want = full - 8 * B * ((N + 1) * (n * n - t(n)) - t(n - 1) + N * (m * m - t(m)))
+        assert packed == want, (packed, want, full)
+
+
+def test_packed_upload_reads_only_lower_triangles_like_the_reference(api, orc):
+    """The reference factorises Q_k and R_k with Eigen's LLT / LDLT, which read
+    the lower triangle (schur.cpp:16), and symmetrises only Q_0 (schur.cpp:56):
+    garbage in the strict upper triangles of Q_k (k >= 1) and R_k changes
+    nothing — on the packed batch path as in the oracle."""
+    B, N, n, m = 6, 31, 14, 7
+    kb = api.random_kkt_batch(5151, B, N, n, m)
+    cfg = PcgConfig(epsilon=1e-8)
+    lam_clean, _ = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg)
+    rng = np.random.default_rng(3)
+    iu = np.triu_indices(n, 1)
+    for s in range(B):
+        for k in range(1, N + 1):
+            kb.Q[s, k][iu] += rng.standard_normal(len(iu[0]))
+        for k in range(N):
+            kb.R[s, k][np.triu_indices(m, 1)] = 1e3
+    lam_dirty, rep = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg)
+    assert np.array_equal(lam_clean, lam_dirty)
+    _, lo, ro = orc.solve_batch(kb, PrecondKind.symmetric_stair, 1, cfg)
+    assert np.array_equal(rep.iterations, np.array([r.iterations for r in ro]))
+    scale = np.maximum(1.0, np.abs(lo).max(axis=1))
+    assert (np.abs(lam_dirty - lo).max(axis=1) / scale).max() <= 1e-10
