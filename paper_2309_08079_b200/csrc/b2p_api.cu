@@ -731,13 +731,33 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     return !small_ok || (K > 24 && (B > 1 || nn == 8));
   };
   const bool one_cta_ok = onecta_n(n) && fused_supported<T>(K, n, k->m, kind);
+  // odd n in [7, 15] on the one-CTA kernel through the identity pad (below)
+  const bool pad_ok = !drift && !dz_dev && sizeof(T) == 8 && (n & 1) && onecta_n(n) && n + 1 <= 16 &&
+                      env_int("B2P_FUSED", 1) && env_int("B2P_PAD", 1) &&
+                      fused_supported<T>(K, n + 1, k->m, kind);
+  const bool small_ok = !drift && env_int("B2P_FUSED", 1) && env_int("B2P_SMALL", 1) &&
+                        small_supported<T>(K, n, k->m, kind) &&
+                        (!dz_dev || small_supported_dz<T>(K, n, k->m, kind));
   // Fused grid kernel: one long-horizon system over G co-resident CTAs (the
   // default for shapes no cluster / one-CTA kernel covers, e.g. c5);
   // B2P_FG=1 forces it, =0 disables it; B2P_FG_RP picks the rows per CTA.
+  // Shapes it is not compiled for run on the smallest compiled (n', m') that
+  // holds them (fp64 n <= 32, m <= 16), through an identity-padded state /
+  // control (Q, R) and zero pads elsewhere — as the one-CTA odd-n pad below:
+  // every pad entry of S, gamma, theta^-1 and the PCG vectors stays exactly 0.
   const int fg_env = env_int("B2P_FG", -1);
-  const int fgRp = (drift || B > 8) ? 0
-                                    : fg_pick_rp<T>(K, n, k->m, kind, c->sm_count,
-                                                    env_int("B2P_FG_RP", 0));
+  int fnp = n, fmp = k->m;
+  // (padded only for shapes no one-CTA / small-block kernel takes, and while
+  // n' <= 2 n: n 4, m 12 on the (32, 16) kernel measured slower than the split
+  // path, scripts/fg_pad_probe.py)
+  const bool fg_shape_ok =
+      !drift && B <= 8 && fg_compiled_shape<T>(n, k->m, &fnp, &fmp) &&
+      ((fnp == n && fmp == k->m) ||
+       (env_int("B2P_FG_PAD", 1) && fnp <= 2 * n && !one_cta_ok && !pad_ok && !small_ok));
+  const int fgRp = !fg_shape_ok ? 0
+                                : fg_pick_rp<T>(K, fnp, fmp, kind, c->sm_count,
+                                                env_int("B2P_FG_RP", 0));
+  const bool fg_padded = fnp != n || fmp != k->m;
   // Single-solve policy (scripts/c1_policy_probe.py, profiles/r02_single_policy.json,
   // and the bench's c1 row): K <= 64 on one CTA (K 64: 87 us vs 93 on the grid
   // kernel; c1: 77 us in the bench vs 88 on the grid kernel there, although an
@@ -746,7 +766,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   const bool single_short = B == 1 && K <= 64 && one_cta_ok;
   const bool use_fg = fgRp > 0 && env_int("B2P_FUSED", 1) &&
                       (fg_env == 1 ||
-                       (fg_env == -1 && ((fcG == 0 && !one_cta_ok) ||
+                       (fg_env == -1 && ((fcG == 0 && !one_cta_ok && !pad_ok) ||
                                          (B == 1 && !single_short && sizeof(T) == 8 &&
                                           fc_env != 1))));
   if (use_fg) {
@@ -765,6 +785,37 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.x0 = static_cast<const T*>(kv.x0);
     f.lambda0 = static_cast<const T*>(lambda0);
     f.lambda_out = static_cast<T*>(lambda_out);
+    T* lam_pad = nullptr;
+    if (fg_padded) {
+      const int m = k->m, N = K - 1, np = fnp, mp = fmp;
+      const long long Bl = B;
+      const size_t eQ = size_t(K) * np * np, eq = size_t(K) * np, eR = size_t(N) * mp * mp,
+                   er = size_t(N) * mp, eA = size_t(N) * np * np, eB = size_t(N) * np * mp,
+                   ee = size_t(N) * np;
+      const size_t per = eQ + eq + eR + er + eA + eB + ee + 2 * np;
+      T* w = static_cast<T*>(ws_get(c, tag + "fgpad_kkt", sizeof(T) * per * B + 256));
+      T *Qp = w, *qp = Qp + eQ * B, *Rp = qp + eq * B, *rp_ = Rp + eR * B, *Ap = rp_ + er * B,
+        *Bp = Ap + eA * B, *ep = Bp + eB * B, *xsp = ep + ee * B, *x0p = xsp + size_t(np) * B;
+      reblock<T>(kv.Q, Qp, Bl * K, n, n, np, np, 1, st);
+      reblock<T>(kv.q, qp, Bl * K, n, 1, np, 1, 0, st);
+      reblock<T>(kv.R, Rp, Bl * N, m, m, mp, mp, 1, st);
+      reblock<T>(kv.r, rp_, Bl * N, m, 1, mp, 1, 0, st);
+      reblock<T>(kv.A, Ap, Bl * N, n, n, np, np, 0, st);
+      reblock<T>(kv.B, Bp, Bl * N, n, m, np, mp, 0, st);
+      reblock<T>(kv.e, ep, Bl * N, n, 1, np, 1, 0, st);
+      reblock<T>(kv.x_s, xsp, Bl, n, 1, np, 1, 0, st);
+      reblock<T>(kv.x0, x0p, Bl, n, 1, np, 1, 0, st);
+      f.Q = Qp, f.q = qp, f.R = Rp, f.r = rp_, f.A = Ap, f.Bm = Bp, f.e = ep, f.x_s = xsp,
+      f.x0 = x0p;
+      lam_pad = static_cast<T*>(ws_get(c, tag + "fgpad_lam", sizeof(T) * B * K * np));
+      if (lambda0) {
+        T* l0p = static_cast<T*>(ws_get(c, tag + "fgpad_l0", sizeof(T) * B * K * np));
+        reblock<T>(lambda0, l0p, Bl * K, n, 1, np, 1, 0, st);
+        f.lambda0 = l0p;
+      }
+      f.lambda_out = lam_pad;
+      c->launches += 9 + (lambda0 ? 1 : 0);
+    }
     f.errkey = errkey;
     f.out = outs_dev;
     f.trace = trace_dev;
@@ -775,7 +826,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     const int G = (K + fgRp - 1) / fgRp;
     FgSync<T> sy{};
     sy.gstride = (G + 31) / 32 * 32;
-    sy.n = n;
+    sy.n = fnp;
     // LL slots: 16 bytes per value. Zeroed when (re)allocated; afterwards each
     // launch starts at a fresh epoch so words of earlier launches never match.
     const size_t slots = static_cast<size_t>(sy.gstride) * (2 * 8 + 2 * 2 * 32);
@@ -823,6 +874,10 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     } else {
       CK(le);
       c->launches++;
+      if (lam_pad) {
+        reblock<T>(lam_pad, lambda_out, static_cast<long long>(B) * K, fnp, 1, n, 1, 0, st);
+        c->launches++;
+      }
       c->last_path = 3;
       c->phases = time_it;
       if (time_it) CK(cudaEventRecord(c->ev1, st));
@@ -886,9 +941,6 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   // S, gamma, theta^-1 and of every PCG vector is then exactly zero, so the
   // real rows follow the unpadded recurrence (the dot products only gain
   // exact zero terms); lambda is cropped back.
-  const bool pad_ok = !drift && !dz_dev && sizeof(T) == 8 && (n & 1) && onecta_n(n) && n + 1 <= 16 &&
-                      env_int("B2P_FUSED", 1) && env_int("B2P_PAD", 1) &&
-                      fused_supported<T>(K, n + 1, k->m, kind);
   if (pad_ok) {
     const int np = n + 1, m = k->m, N = K - 1;
     const long long Bl = B;

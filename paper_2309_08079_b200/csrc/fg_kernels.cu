@@ -691,17 +691,49 @@ template <class T, int NB, int MB>
 size_t fg_smem(int rp) {
   return sizeof(T) * static_cast<size_t>(FgLayout<T, NB, MB>::total(rp));
 }
+// compiled shapes: the BASELINE ones exactly, plus (16, 8) and (32, 16) that
+// every other fp64 shape with n <= 32, m <= 16 runs on through identity / zero
+// pads (fg_compiled_shape, the host side pads)
 template <class T>
 bool fg_shape(int n, int m) {
-  if (sizeof(T) == 8) return (n == 28 && m == 14) || (n == 14 && m == 7);
+  if (sizeof(T) == 8)
+    return (n == 28 && m == 14) || (n == 14 && m == 7) || (n == 16 && m == 8) || (n == 32 && m == 16);
   return n == 12 && m == 4;
 }
 template <class T>
 size_t fg_smem_rt(int n, int m, int rp) {
-  if (sizeof(T) == 8) return n == 28 ? fg_smem<T, 28, 14>(rp) : fg_smem<T, 14, 7>(rp);
+  if (sizeof(T) == 8) {
+    switch (n) {
+      case 28: return fg_smem<T, 28, 14>(rp);
+      case 16: return fg_smem<T, 16, 8>(rp);
+      case 32: return fg_smem<T, 32, 16>(rp);
+      default: return fg_smem<T, 14, 7>(rp);
+    }
+  }
   return fg_smem<T, 12, 4>(rp);
 }
 }  // namespace
+
+template <class T>
+bool fg_compiled_shape(int n, int m, int* np, int* mp) {
+  if (fg_shape<T>(n, m)) {
+    *np = n;
+    *mp = m;
+    return true;
+  }
+  if (sizeof(T) != 8 || n < 1 || m < 1) return false;
+  if (n <= 16 && m <= 8) {
+    *np = 16;
+    *mp = 8;
+    return true;
+  }
+  if (n <= 32 && m <= 16) {
+    *np = 32;
+    *mp = 16;
+    return true;
+  }
+  return false;
+}
 
 template <class T>
 int fg_pick_rp(int K, int n, int m, int kind, int sm_count, int want_rp) {
@@ -738,13 +770,19 @@ cudaError_t launch_fg(const FusedParams<T>& p, const FgSync<T>& sy, int rp, cuda
                                        args, smem, st);
   };
   if constexpr (sizeof(T) == 8) {
-    if (sy.n == 28) return go(k_fg<T, 28, 14>, fg_smem<T, 28, 14>(rp));
-    return go(k_fg<T, 14, 7>, fg_smem<T, 14, 7>(rp));
+    switch (sy.n) {
+      case 28: return go(k_fg<T, 28, 14>, fg_smem<T, 28, 14>(rp));
+      case 16: return go(k_fg<T, 16, 8>, fg_smem<T, 16, 8>(rp));
+      case 32: return go(k_fg<T, 32, 16>, fg_smem<T, 32, 16>(rp));
+      default: return go(k_fg<T, 14, 7>, fg_smem<T, 14, 7>(rp));
+    }
   } else {
     return go(k_fg<T, 12, 4>, fg_smem<T, 12, 4>(rp));
   }
 }
 
+template bool fg_compiled_shape<double>(int, int, int*, int*);
+template bool fg_compiled_shape<float>(int, int, int*, int*);
 template int fg_pick_rp<double>(int, int, int, int, int, int);
 template int fg_pick_rp<float>(int, int, int, int, int, int);
 template cudaError_t launch_fg<double>(const FusedParams<double>&, const FgSync<double>&, int,

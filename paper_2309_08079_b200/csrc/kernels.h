@@ -124,6 +124,8 @@ struct FgSync {
   unsigned epoch0;  // first epoch of this launch (flags of older launches never match)
 };
 template <class T> int fg_pick_rp(int K, int n, int m, int kind, int sm_count, int want_rp);
+// the grid kernel's compiled shape that holds (n, m) (itself, or a padded one)
+template <class T> bool fg_compiled_shape(int n, int m, int* np, int* mp);
 template <class T>
 cudaError_t launch_fg(const FusedParams<T>& p, const FgSync<T>& sy, int rp, cudaStream_t st);
 

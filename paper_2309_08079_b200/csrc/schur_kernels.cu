@@ -35,7 +35,7 @@ struct FormLayout {
     oAQ = o; o += tn;
     oBR = o; o += tnm;
     oT = o; o += tn;
-    oW = o; o += tn;
+    oW = o; o += tn > tm ? tn : tm;  // also the R_k factorisation scratch (m > n)
     vq = o; o += 32;
     vr = o; o += 32;
     vq1 = o; o += 32;

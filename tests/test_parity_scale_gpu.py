@@ -175,14 +175,14 @@ def test_packed_upload_equals_full_blocks(api, env, shape):
     B = 96
     kb = api.random_kkt_batch(4242 + n, B, N, n, m)
     cfg = PcgConfig(epsilon=1e-8)
-    env["B2P_PACK_SYM"] = "0"
-    ctx = api.Context(0)
-    lam0, rep0 = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg, ctx=ctx)
-    full = ctx.last_h2d_bytes()
-    ctx.close()
-    env["B2P_PACK_SYM"] = "1"
-    for chunk in ("512", "7"):
+    for chunk in ("512", "7"):  # (chunks of <= 8 systems may take another kernel)
         env["B2P_BATCH_CHUNK"] = chunk
+        env["B2P_PACK_SYM"] = "0"
+        ctx = api.Context(0)
+        lam0, rep0 = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg, ctx=ctx)
+        full = ctx.last_h2d_bytes()
+        ctx.close()
+        env["B2P_PACK_SYM"] = "1"
         ctx = api.Context(0)
         lam1, rep1 = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg, ctx=ctx)
         packed = ctx.last_h2d_bytes()
