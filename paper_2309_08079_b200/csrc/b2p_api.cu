@@ -738,6 +738,18 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   const bool small_ok = !drift && env_int("B2P_FUSED", 1) && env_int("B2P_SMALL", 1) &&
                         small_supported<T>(K, n, k->m, kind) &&
                         (!dz_dev || small_supported_dz<T>(K, n, k->m, kind));
+  // Batches of n in [11, 16], m <= 8 that neither the one-CTA kernel (K > 64) nor
+  // the small-block kernel takes: the cluster kernel compiled at (16, 8)
+  // through the same pads (B2P_FC_PAD=0 disables). scripts/fc_pad_probe.py:
+  // 4096 x K 128 n12 m4 98 K -> 214 K/s, K 65 n14 m5 141 K -> 303 K/s vs the
+  // split path; n 9 (16 / 9 of the state) measured equal, so it stays split.
+  int cnp = n, cmp = k->m;
+  if (fcG == 0 && !drift && sizeof(T) == 8 && n >= 11 && n <= 16 && k->m >= 1 && k->m <= 8 &&
+      !one_cta_ok && !pad_ok && !small_ok && env_int("B2P_FC_PAD", 1)) {
+    fcG = fc_pick_g<T>(K, 16, 8, kind, B);
+    if (fcG > 0) cnp = 16, cmp = 8;
+  }
+  const bool fc_padded = cnp != n || cmp != k->m;
   // Fused grid kernel: one long-horizon system over G co-resident CTAs (the
   // default for shapes no cluster / one-CTA kernel covers, e.g. c5);
   // B2P_FG=1 forces it, =0 disables it; B2P_FG_RP picks the rows per CTA.
@@ -769,6 +781,40 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
                        (fg_env == -1 && ((fcG == 0 && !one_cta_ok && !pad_ok) ||
                                          (B == 1 && !single_short && sizeof(T) == 8 &&
                                           fc_env != 1))));
+  // Identity-padded Q / R and zero-padded A, B, q, r, e, x_s, x0 (and lambda0)
+  // at (np, mp) for the grid / cluster kernels' compiled shapes; points f at
+  // them and returns the padded lambda the caller crops back.
+  auto pad_view = [&](int np, int mp, FusedParams<T>& f) -> T* {
+    const int m = k->m, N = K - 1;
+    const long long Bl = B;
+    const size_t eQ = size_t(K) * np * np, eq = size_t(K) * np, eR = size_t(N) * mp * mp,
+                 er = size_t(N) * mp, eA = size_t(N) * np * np, eB = size_t(N) * np * mp,
+                 ee = size_t(N) * np;
+    const size_t per = eQ + eq + eR + er + eA + eB + ee + 2 * np;
+    T* w = static_cast<T*>(ws_get(c, tag + "xpad_kkt", sizeof(T) * per * B + 256));
+    T *Qp = w, *qp = Qp + eQ * B, *Rp = qp + eq * B, *rp_ = Rp + eR * B, *Ap = rp_ + er * B,
+      *Bp = Ap + eA * B, *ep = Bp + eB * B, *xsp = ep + ee * B, *x0p = xsp + size_t(np) * B;
+    reblock<T>(kv.Q, Qp, Bl * K, n, n, np, np, 1, st);
+    reblock<T>(kv.q, qp, Bl * K, n, 1, np, 1, 0, st);
+    reblock<T>(kv.R, Rp, Bl * N, m, m, mp, mp, 1, st);
+    reblock<T>(kv.r, rp_, Bl * N, m, 1, mp, 1, 0, st);
+    reblock<T>(kv.A, Ap, Bl * N, n, n, np, np, 0, st);
+    reblock<T>(kv.B, Bp, Bl * N, n, m, np, mp, 0, st);
+    reblock<T>(kv.e, ep, Bl * N, n, 1, np, 1, 0, st);
+    reblock<T>(kv.x_s, xsp, Bl, n, 1, np, 1, 0, st);
+    reblock<T>(kv.x0, x0p, Bl, n, 1, np, 1, 0, st);
+    f.Q = Qp, f.q = qp, f.R = Rp, f.r = rp_, f.A = Ap, f.Bm = Bp, f.e = ep, f.x_s = xsp,
+    f.x0 = x0p;
+    T* lam_pad = static_cast<T*>(ws_get(c, tag + "xpad_lam", sizeof(T) * B * K * np));
+    if (lambda0) {
+      T* l0p = static_cast<T*>(ws_get(c, tag + "xpad_l0", sizeof(T) * B * K * np));
+      reblock<T>(lambda0, l0p, Bl * K, n, 1, np, 1, 0, st);
+      f.lambda0 = l0p;
+    }
+    f.lambda_out = lam_pad;
+    c->launches += 9 + (lambda0 ? 1 : 0);
+    return lam_pad;
+  };
   if (use_fg) {
     FusedParams<T> f{};
     f.B = B;
@@ -785,37 +831,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.x0 = static_cast<const T*>(kv.x0);
     f.lambda0 = static_cast<const T*>(lambda0);
     f.lambda_out = static_cast<T*>(lambda_out);
-    T* lam_pad = nullptr;
-    if (fg_padded) {
-      const int m = k->m, N = K - 1, np = fnp, mp = fmp;
-      const long long Bl = B;
-      const size_t eQ = size_t(K) * np * np, eq = size_t(K) * np, eR = size_t(N) * mp * mp,
-                   er = size_t(N) * mp, eA = size_t(N) * np * np, eB = size_t(N) * np * mp,
-                   ee = size_t(N) * np;
-      const size_t per = eQ + eq + eR + er + eA + eB + ee + 2 * np;
-      T* w = static_cast<T*>(ws_get(c, tag + "fgpad_kkt", sizeof(T) * per * B + 256));
-      T *Qp = w, *qp = Qp + eQ * B, *Rp = qp + eq * B, *rp_ = Rp + eR * B, *Ap = rp_ + er * B,
-        *Bp = Ap + eA * B, *ep = Bp + eB * B, *xsp = ep + ee * B, *x0p = xsp + size_t(np) * B;
-      reblock<T>(kv.Q, Qp, Bl * K, n, n, np, np, 1, st);
-      reblock<T>(kv.q, qp, Bl * K, n, 1, np, 1, 0, st);
-      reblock<T>(kv.R, Rp, Bl * N, m, m, mp, mp, 1, st);
-      reblock<T>(kv.r, rp_, Bl * N, m, 1, mp, 1, 0, st);
-      reblock<T>(kv.A, Ap, Bl * N, n, n, np, np, 0, st);
-      reblock<T>(kv.B, Bp, Bl * N, n, m, np, mp, 0, st);
-      reblock<T>(kv.e, ep, Bl * N, n, 1, np, 1, 0, st);
-      reblock<T>(kv.x_s, xsp, Bl, n, 1, np, 1, 0, st);
-      reblock<T>(kv.x0, x0p, Bl, n, 1, np, 1, 0, st);
-      f.Q = Qp, f.q = qp, f.R = Rp, f.r = rp_, f.A = Ap, f.Bm = Bp, f.e = ep, f.x_s = xsp,
-      f.x0 = x0p;
-      lam_pad = static_cast<T*>(ws_get(c, tag + "fgpad_lam", sizeof(T) * B * K * np));
-      if (lambda0) {
-        T* l0p = static_cast<T*>(ws_get(c, tag + "fgpad_l0", sizeof(T) * B * K * np));
-        reblock<T>(lambda0, l0p, Bl * K, n, 1, np, 1, 0, st);
-        f.lambda0 = l0p;
-      }
-      f.lambda_out = lam_pad;
-      c->launches += 9 + (lambda0 ? 1 : 0);
-    }
+    T* lam_pad = fg_padded ? pad_view(fnp, fmp, f) : nullptr;
     f.errkey = errkey;
     f.out = outs_dev;
     f.trace = trace_dev;
@@ -904,7 +920,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     // keyed by the stream tag: chunks on two streams may run concurrently and
     // each CTA owns the slot at its blockIdx
     f.slot = static_cast<T*>(ws_get(c, tag + "fc_slot", sizeof(T) * fcG * max_clusters *
-                                                       fc_slot_elems<T>(K, n, fcG)));
+                                                       fc_slot_elems<T>(K, cnp, fcG)));
     f.lambda0 = static_cast<const T*>(lambda0);
     f.lambda_out = static_cast<T*>(lambda_out);
     f.errkey = errkey;
@@ -929,8 +945,13 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       CK(cudaEventRecord(c->ev0, st));
       CK(cudaEventRecord(c->ev2, st));
     }
-    CK(launch_fc<T>(f, fcG, max_clusters, st));
+    T* lam_pad = fc_padded ? pad_view(cnp, cmp, f) : nullptr;
+    CK(launch_fc<T>(f, fcG, max_clusters, st, cnp));
     c->launches++;
+    if (lam_pad) {
+      reblock<T>(lam_pad, lambda_out, static_cast<long long>(B) * K, cnp, 1, n, 1, 0, st);
+      c->launches++;
+    }
     c->last_path = 2;
     c->phases = time_it;
     if (time_it) CK(cudaEventRecord(c->ev1, st));

@@ -521,7 +521,9 @@ size_t fc_smem(int rp) {
 
 template <class T>
 int fc_pick_g(int K, int n, int m, int kind, int B) {
-  const bool shape = (sizeof(T) == 8 && n == 14 && m == 7) || (sizeof(T) == 4 && n == 12 && m == 4);
+  // compiled: (14, 7), (16, 8) fp64 (the latter for padded shapes), (12, 4) fp32
+  const bool shape = (sizeof(T) == 8 && ((n == 14 && m == 7) || (n == 16 && m == 8))) ||
+                     (sizeof(T) == 4 && n == 12 && m == 4);
   if (!shape || kind == kPoly || K < 2) return 0;
   for (int G : {1, 2, 4, 8, 16}) {
     const int rp = (K + G - 1) / G;
@@ -537,7 +539,7 @@ size_t fc_slot_elems(int K, int n, int G) {
 }
 
 template <class T>
-cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStream_t st) {
+cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStream_t st, int nb) {
   const int rp = (p.K + G - 1) / G;
   auto go = [&](auto kern, size_t smem) -> cudaError_t {
     cudaError_t e = ensure_max_smem(kern, smem);
@@ -566,6 +568,7 @@ cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStre
     return cudaLaunchKernelEx(&cfg, kern, p, rp);
   };
   if constexpr (sizeof(T) == 8) {
+    if (nb == 16) return go(k_fc<T, 16, 8>, fc_smem<T, 16, 8>(rp));
     return go(k_fc<T, 14, 7>, fc_smem<T, 14, 7>(rp));
   } else {
     return go(k_fc<T, 12, 4>, fc_smem<T, 12, 4>(rp));
@@ -576,7 +579,7 @@ template int fc_pick_g<double>(int, int, int, int, int);
 template int fc_pick_g<float>(int, int, int, int, int);
 template size_t fc_slot_elems<double>(int, int, int);
 template size_t fc_slot_elems<float>(int, int, int);
-template cudaError_t launch_fc<double>(const FusedParams<double>&, int, int, cudaStream_t);
-template cudaError_t launch_fc<float>(const FusedParams<float>&, int, int, cudaStream_t);
+template cudaError_t launch_fc<double>(const FusedParams<double>&, int, int, cudaStream_t, int);
+template cudaError_t launch_fc<float>(const FusedParams<float>&, int, int, cudaStream_t, int);
 
 }  // namespace b2p

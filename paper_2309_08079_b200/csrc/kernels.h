@@ -109,7 +109,7 @@ cudaError_t launch_small(const FusedParams<T>& p, int n, int m, int grid, cudaSt
 template <class T> int fc_pick_g(int K, int n, int m, int kind, int B);
 template <class T> size_t fc_slot_elems(int K, int n, int G);
 template <class T>
-cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStream_t st);
+cudaError_t launch_fc(const FusedParams<T>& p, int G, int max_clusters, cudaStream_t st, int nb);
 
 // Fused grid kernel (fg_kernels.cu): one long-horizon system on G co-resident
 // CTAs (cooperative launch) of rp block rows each. FgSync is the zeroed global

@@ -107,3 +107,20 @@ def test_split_path_control_wider_than_state(api, orc, env, N, n, m):
     want = orc.solve(kkt, PrecondKind.symmetric_stair, cfg=cfg)
     assert got.report.iterations == want.report.iterations
     assert rel_inf_error(got.lambda_, want.lambda_) <= TOL64
+
+
+@pytest.mark.parametrize("K,n,m,B", [(128, 12, 4, 24), (100, 11, 3, 16), (256, 16, 8, 12),
+                                     (65, 14, 5, 20), (80, 15, 8, 9)])
+def test_padded_cluster_batches_match_oracle(api, orc, K, n, m, B):
+    """Batches of n in [11, 16], m <= 8 at horizons the one-CTA kernel cannot
+    hold (K > 64): the cluster kernel compiled at (16, 8) through the same
+    identity / zero pads; per-system iteration counts and lambda."""
+    kb = api.random_kkt_batch(9600 + K + n + m, B, K - 1, n, m)
+    cfg = PcgConfig(epsilon=1e-8)
+    for kind in (PrecondKind.symmetric_stair, PrecondKind.block_jacobi):
+        lam, reps = api.solve_batched(kb, kind, 1, cfg)
+        assert api.context().last_path() == 2  # the fused cluster kernel
+        _, lo, ro = orc.solve_batch(kb, kind, 1, cfg)
+        assert np.array_equal(reps.iterations, np.array([r.iterations for r in ro]))
+        scale = np.maximum(1.0, np.abs(lo).max(axis=1))
+        assert (np.abs(lam - lo).max(axis=1) / scale).max() <= TOL64
