@@ -157,9 +157,11 @@ int guard(b2p_error* err, F&& f) {
     f();
     return B2P_OK;
   } catch (const Fail& e) {
+    (void)cudaGetLastError();  // a failed launch must not surface in the next call
     fill_err(err, e);
     return e.code;
   } catch (const std::exception& e) {
+    (void)cudaGetLastError();
     fill_err(err, Fail{B2P_RUNTIME_ERROR, e.what()});
     return B2P_RUNTIME_ERROR;
   }
@@ -350,8 +352,16 @@ void configure_pcg(b2p_ctx* c, PcgParams<T>& p, bool allow_grid) {
       }
     }
   }
-  try_cfg(1, 0);
-  p.sync = kSyncCta;
+  // unstaged (S rows read from global memory): the smallest CTA group whose
+  // vector slices fit — long horizons of large blocks need a cluster even so
+  for (int G : {1, 2, 4, 8, 16}) {
+    if (!try_cfg(G, 0)) continue;
+    set_sync();
+    if (p.sync == kSyncGrid && (!allow_grid || p.B > 1)) continue;
+    return;
+  }
+  throw Fail{B2P_RUNTIME_ERROR, "pcg: the PCG vectors of one system (K = " + std::to_string(p.K) +
+                                    ", n = " + std::to_string(p.nb) + ") exceed 16 CTAs' shared memory"};
 }
 
 template <class T>

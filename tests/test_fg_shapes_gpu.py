@@ -124,3 +124,35 @@ def test_padded_cluster_batches_match_oracle(api, orc, K, n, m, B):
         assert np.array_equal(reps.iterations, np.array([r.iterations for r in ro]))
         scale = np.maximum(1.0, np.abs(lo).max(axis=1))
         assert (np.abs(lam - lo).max(axis=1) / scale).max() <= TOL64
+
+
+def test_split_path_large_blocks_long_horizon_batch_and_error_isolation(api, orc):
+    """B = 9 systems of K 201, n 27, m 16 (beyond every fused kernel): the split
+    PCG's vector slices exceed one CTA's shared memory unstaged too, so it runs
+    on a cluster; then an unrelated fp32 solve on the same context (a failed
+    launch must never surface in the next call)."""
+    kb = api.random_kkt_batch(9701, 9, 200, 27, 16)
+    cfg = PcgConfig(epsilon=1e-8)
+    lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, cfg)
+    _, lo, ro = orc.solve_batch(kb, PrecondKind.symmetric_stair, 1, cfg)
+    assert np.array_equal(reps.iterations, np.array([r.iterations for r in ro]))
+    scale = np.maximum(1.0, np.abs(lo).max(axis=1))
+    assert (np.abs(lam - lo).max(axis=1) / scale).max() <= TOL64
+    k32 = orc.random_kkt(9702, 63, 11, 4)
+    got = api.solve(k32, PrecondKind.stair, cfg=PcgConfig(epsilon=1e-4), dtype=np.float32)
+    want = orc.solve(k32, PrecondKind.stair, cfg=PcgConfig(epsilon=1e-4))
+    assert abs(got.report.iterations - want.report.iterations) <= 1
+
+
+def test_randomised_shapes_every_path(api, orc):
+    """scripts/shape_fuzz.py's sweep, bounded: (N, n, m, B, kind, dtype) drawn
+    across every kernel path's bounds; each system against the oracle."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "shape_fuzz.py"), "60", "11"],
+                         capture_output=True, text=True, timeout=900)
+    import json
+    last = json.loads(out.stdout.strip().splitlines()[-1])
+    assert last["failed"] == 0, last["bad"]
+    assert len(last["paths"]) >= 4, last["paths"]  # the sweep reached most kernel paths
