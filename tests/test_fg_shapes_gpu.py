@@ -156,3 +156,17 @@ def test_randomised_shapes_every_path(api, orc):
     last = json.loads(out.stdout.strip().splitlines()[-1])
     assert last["failed"] == 0, last["bad"]
     assert len(last["paths"]) >= 4, last["paths"]  # the sweep reached most kernel paths
+
+
+def test_randomised_shapes_rest_of_the_api(api, orc):
+    """scripts/api_fuzz.py, bounded: build_schur, build / apply_preconditioner,
+    the explicit-Phi pcg_solve_auto, reconstruct_primal and sqp_step over
+    random (N, n <= 32, m <= 16) against the oracle."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "api_fuzz.py"), "30", "12"],
+                         capture_output=True, text=True, timeout=900)
+    last = json.loads(out.stdout.strip().splitlines()[-1])
+    assert last["failed"] == 0, last["bad"]
