@@ -359,7 +359,10 @@ __global__ void __launch_bounds__(kFcThreads, 1) k_fc(FusedParams<T> p, int rp) 
     T* const rmR = rhalo ? cl.map_shared_rank(sm, c + 1) : sm;
     T* myP = sP + (h + 1) * VS;  // p row b
 
+    // (half-warps past the CTA's last row compute nothing: their rows would
+    // index past the row arrays, into buffers other warps are writing)
     auto Srow = [&](const T* P) -> T {  // ((D p_b + L p_{b-1}) + R p_{b+1}), block_tri.cpp:82-92
+      if (!rowv) return T(0);
       const T* pb = P + (h + 1) * VS;
       T out = dot_row<T, NB>(sD + h * NN + lr * NB, pb);
       if (hasL) out += dot_reg<T, NB>(lrow, pb - VS);
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) k_fc(FusedParams<T> p, int rp) 
       if (p.kind == kIdentity) return rv;
       if (act) sU[h * VS + l] = rv;
       __syncwarp();
-      const T tv = dot_reg<T, NB>(ti, sU + h * VS);  // t = theta^-1 r
+      const T tv = rowv ? dot_reg<T, NB>(ti, sU + h * VS) : T(0);  // t = theta^-1 r
       if (!stairish) return tv;                     // block Jacobi
       if (act) sT[h * VS + l] = tv;
       if (G == 1) __syncthreads(); else cl.sync();
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(kFcThreads, 1) k_fc(FusedParams<T> p, int rp) 
       if (act) sU[h * VS + l] = uv;
       __syncwarp();
       const bool corr = (p.kind == kSymStair) || (b & 1);
-      return corr ? dot_reg<T, NB>(ti, sU + h * VS) : tv;  // r~ = theta^-1 u
+      return (corr && rowv) ? dot_reg<T, NB>(ti, sU + h * VS) : tv;  // r~ = theta^-1 u
     };
 
     // r = gamma - S lambda0 (pcg.cpp:62)

@@ -76,3 +76,14 @@ print("batched one-CTA n7 padded", api.context().last_path(), [x.iterations for 
 k8 = api.random_kkt(19, 39, 8, 4)
 res, dz8 = api.sqp_step(k8, cfg=cfg)
 print("one-CTA n8 sqp_step", api.context().last_path(), res.report.iterations)
+# padded grid / cluster shapes and the packed host batch upload
+kp = api.random_kkt(20, 99, 20, 10)
+r = api.solve(kp, cfg=cfg)
+print("padded grid (20, 10)", api.context().last_path(), r.report.iterations)
+kb = api.random_kkt_batch(21, 9, 79, 12, 4)
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("padded cluster (12, 4) K 80", api.context().last_path(), [x.iterations for x in reps])
+os.environ["B2P_BATCH_CHUNK"] = "5"
+kb = api.random_kkt_batch(22, 12, 31, 14, 7)
+lam, reps = api.solve_batched(kb, cfg=cfg)
+print("packed upload, chunks of 5", api.context().last_path(), [x.iterations for x in reps])
