@@ -761,7 +761,7 @@ def run_b200(a, world, rank, local):
                  "all_ok": bool((status == -1).all().item()),
                  "max_rel_diff_vs_pcg": rel,
                  "what": "b2p_direct_solve_batched_device: build_schur + block-Thomas "
-                         "cholesky_solve (block_tri.cpp:121-159), one warp per system, on the "
+                         "cholesky_solve (block_tri.cpp:121-159), a half-warp per system, on the "
                          "bench batch; the PCG solves stop at eta' < eps, hence the difference"}
 
     # ---- roofline of the dominant kernel (one launch per step = the whole step)

@@ -11,6 +11,8 @@
 // and no inter-row synchronisation is needed.
 #include <climits>
 
+#include <cstdlib>
+
 #include "kernels.h"
 #include "warp_dense.cuh"
 
@@ -456,6 +458,216 @@ __global__ void k_block_cholesky(int K, int nb, const T* __restrict__ M, const T
   if (lane == 0) *status = -1;
 }
 
+// Block Thomas (BlockTriMatrix::cholesky_solve, block_tri.cpp:121-159) with the
+// block dimension a compile-time constant: a half-warp per system (lane l < NB
+// owns row l; lane NB carries the vector right-hand side through the block
+// solves), the factor of Dhat_{i-1} and its reciprocal diagonal in shared
+// memory, the next step's blocks prefetched into registers. Latency-bound by
+// the 2 K dependent block factorisations / solves per system, so every system
+// of a batch runs concurrently (28 per SM at c4). Same factorisation and block
+// order as the reference; within-block association differs (column sweeps),
+// so results agree to rounding (tests: 1e-10 of the oracle's cholesky_solve).
+template <class T, int NB>
+__global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* __restrict__ M,
+                                                         const T* __restrict__ rhs, T* __restrict__ x,
+                                                         T* __restrict__ factors, T* __restrict__ y,
+                                                         int* __restrict__ status) {
+  static_assert(NB >= 1 && NB < 16, "one half-warp lane per row plus the vector lane");
+  constexpr int LD = NB + 1, NN = NB * NB, TS = NB * LD;
+  __shared__ T sm[4][3 * TS + 2 * 16];
+  const int hw = threadIdx.x >> 4, l = threadIdx.x & 15;
+  const unsigned mask = 0xffffu << (16 * ((threadIdx.x >> 4) & 1));
+  const int sys = blockIdx.x * 4 + hw;
+  if (sys >= B) return;  // whole half-warps
+  T* F = sm[hw];        // factor of Dhat_{i-1} (lower, row-major, ld LD)
+  T* W = F + TS;        // Dhat_i, factorised in place (then swapped with F)
+  T* X = W + TS;        // Dhat_{i-1}^-1 [L_i' | y_{i-1}]: column j = lane j
+  T* rdF = X + TS;      // 1 / F(r, r)
+  T* rdW = rdF + 16;    // 1 / W(r, r)
+  const size_t D = static_cast<size_t>(K) * NB;
+  M += static_cast<size_t>(sys) * K * 3 * NN;
+  rhs += sys * D;
+  x += sys * D;
+  y += sys * D;
+  factors += static_cast<size_t>(sys) * K * NN;
+  status += sys;
+  const bool row = l < NB;
+  const int lr = row ? l : NB - 1;
+  auto blk = [&](int r, int s_) { return M + (static_cast<size_t>(r) * 3 + s_) * NN; };
+  // In-place left-looking Cholesky of W (lane l: row l), Eigen's llt order;
+  // returns the failing pivot (half-warp uniform) or -1.
+  auto chol = [&](T* A, T* rd) -> int {
+    int fail = -1;
+#pragma unroll 1
+    for (int k = 0; k < NB; ++k) {
+      T s = A[lr * LD + k];
+#pragma unroll 4
+      for (int q = 0; q < k; ++q) s -= A[lr * LD + q] * A[k * LD + q];
+      const T piv = __shfl_sync(mask, s, k, 16);
+      if (piv <= T(0) && fail < 0) fail = k;  // x <= 0 fails, NaN passes (Eigen LLT)
+      const T sq = sqrt(piv <= T(0) ? T(1) : piv);
+      const T rk = T(1) / sq;  // one division per pivot
+      __syncwarp(mask);
+      if (row && l >= k) A[l * LD + k] = l == k ? sq : s * rk;
+      if (l == k) rd[k] = rk;
+      __syncwarp(mask);
+    }
+    return fail;
+  };
+  // F F' z = b for the calling lane's column b of X (in place, shared memory)
+  auto col_solve = [&](T* Z, const T* Fm, const T* rd) {
+    T z[NB];  // the column, kept in registers through both sweeps
+#pragma unroll
+    for (int r = 0; r < NB; ++r) z[r] = Z[r * LD];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      T s = z[r];
+#pragma unroll
+      for (int q = 0; q < r; ++q) s -= Fm[r * LD + q] * z[q];
+      z[r] = s * rd[r];
+    }
+#pragma unroll
+    for (int r = NB - 1; r >= 0; --r) {
+      T s = z[r];
+#pragma unroll
+      for (int q = r + 1; q < NB; ++q) s -= Fm[q * LD + r] * z[q];
+      z[r] = s * rd[r];
+    }
+#pragma unroll
+    for (int r = 0; r < NB; ++r) Z[r * LD] = z[r];
+  };
+  // F F' v = b for one vector held as v (lane l: element l): column sweeps with
+  // shuffles, the whole half-warp in step
+  auto vec_solve = [&](T v, const T* Fm, const T* rd) -> T {
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const T zr = __shfl_sync(mask, v, r, 16) * rd[r];
+      v = l == r ? zr : (l > r && row ? v - Fm[lr * LD + r] * zr : v);
+    }
+#pragma unroll
+    for (int r = NB - 1; r >= 0; --r) {
+      const T xr = __shfl_sync(mask, v, r, 16) * rd[r];
+      v = l == r ? xr : (l < r ? v - Fm[r * LD + lr] * xr : v);
+    }
+    return v;
+  };
+  auto pf = [&](const T* p0) {  // L2 prefetch of row l of a block
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + lr * NB));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + lr * NB + NB - 1));
+  };
+  // block 0
+  if (row)
+    for (int j = 0; j < NB; ++j) F[l * LD + j] = blk(0, 1)[l * NB + j];
+  T yv = row ? rhs[l] : T(0);
+  if (K > 1) {
+    pf(blk(1, 0));
+    pf(blk(1, 1));
+  }
+  __syncwarp(mask);
+  if (chol(F, rdF) >= 0) {
+    if (l == 0) *status = 0;
+    return;
+  }
+  if (row) {
+    for (int j = 0; j < NB; ++j) factors[l * NB + j] = F[l * LD + j];
+    y[l] = yv;
+  }
+  for (int i = 1; i < K; ++i) {
+    // X = Dhat_{i-1}^-1 [L_i' | y_{i-1}]: lane j < NB column j (row j of L_i),
+    // lane NB the vector y_{i-1} (from the lanes holding it); L_i's rows also
+    // parked in W (scratch until Dhat_i) so they are not live in registers
+    // through the solves
+    {
+      const T* Li = blk(i, 0) + lr * NB;
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const T v = Li[q];
+        const T yq = __shfl_sync(mask, yv, q, 16);
+        if (row) {
+          X[q * LD + l] = v;
+          W[l * LD + q] = v;
+        }
+        if (l == NB) X[q * LD + NB] = yq;
+      }
+    }
+    if (i + 1 < K) {
+      pf(blk(i + 1, 0));
+      pf(blk(i + 1, 1));
+    }
+    if (row || l == NB) col_solve(X + l, F, rdF);
+    __syncwarp(mask);
+    T Lrow[NB];  // row l of L_i
+#pragma unroll
+    for (int q = 0; q < NB; ++q) Lrow[q] = row ? W[l * LD + q] : T(0);
+    // y_i = rhs_i - L_i X[:, NB]; Dhat_i = D_i - L_i X[:, :NB] (into W)
+    T yi = row ? rhs[static_cast<size_t>(i) * NB + l] : T(0);
+    {
+      T sy = T(0);
+#pragma unroll
+      for (int q = 0; q < NB; ++q) sy += Lrow[q] * X[q * LD + NB];
+      yi -= sy;
+    }
+    const T* Dr = blk(i, 1) + lr * NB;
+#pragma unroll 2
+    for (int j = 0; j < NB; ++j) {
+      T s = T(0);
+#pragma unroll
+      for (int q = 0; q < NB; ++q) s += Lrow[q] * X[q * LD + j];
+      if (row) W[l * LD + j] = Dr[j] - s;
+    }
+    __syncwarp(mask);
+    if (chol(W, rdW) >= 0) {
+      if (l == 0) *status = i;
+      return;
+    }
+    yv = yi;
+    if (row) {
+      T* Fo = factors + static_cast<size_t>(i) * NN;
+      for (int j = 0; j < NB; ++j) Fo[l * NB + j] = W[l * LD + j];
+      y[static_cast<size_t>(i) * NB + l] = yi;
+    }
+    {  // W becomes the factor of Dhat_i
+      T* t = F;
+      F = W;
+      W = t;
+      t = rdF;
+      rdF = rdW;
+      rdW = t;
+    }
+    __syncwarp(mask);
+  }
+  // back substitution: x_i = Dhat_i^-1 (y_i - R_i x_{i+1}); F holds Dhat_{K-1}
+  T* xs = X;  // x_{i+1} for the R_i row products (shared by the half-warp)
+  T xv = vec_solve(yv, F, rdF);  // lane l: element l of x_{K-1}
+  for (int i = K - 2; i >= -1; --i) {
+    if (row) x[static_cast<size_t>(i + 1) * NB + l] = xv;
+    if (i < 0) break;
+    __syncwarp(mask);
+    if (i > 0) {  // the next step's factor and R rows into L2
+      pf(factors + static_cast<size_t>(i - 1) * NN);
+      pf(blk(i - 1, 2));
+    }
+    if (row) {
+      xs[l] = xv;
+      const T* Fi = factors + static_cast<size_t>(i) * NN;  // F <- factor i
+      for (int j = 0; j < NB; ++j) F[l * LD + j] = Fi[l * NB + j];
+      rdF[l] = T(1) / Fi[l * NB + l];
+    }
+    __syncwarp(mask);
+    T v = T(0);
+    if (row) {
+      const T* Rb = blk(i, 2) + l * NB;
+      T s = T(0);
+#pragma unroll
+      for (int q = 0; q < NB; ++q) s += Rb[q] * xs[q];
+      v = y[static_cast<size_t>(i) * NB + l] - s;
+    }
+    __syncwarp(mask);
+    xv = vec_solve(v, F, rdF);
+  }
+  if (l == 0) *status = -1;
+}
+
 // ----------------------------------------------------------------- launchers
 template <class T>
 cudaError_t launch_build_schur(const FormParams<T>& p, cudaStream_t st) {
@@ -508,6 +720,10 @@ cudaError_t launch_blocktri_check(int K, int nb, const T* M, double* out2, cudaS
 template <class T>
 cudaError_t launch_block_cholesky(int B, int K, int nb, const T* M, const T* rhs, T* x, T* factors,
                                   T* y, int* status, cudaStream_t st) {
+  if (nb == 14 && K >= 1 && !std::getenv("B2P_DIRECT_WARP")) {  // the c4 / c1 block dimension
+    k_block_thomas<T, 14><<<(B + 3) / 4, 64, 0, st>>>(B, K, M, rhs, x, factors, y, status);
+    return cudaGetLastError();
+  }
   const int ld = tile_ld(nb);
   const size_t smem = sizeof(T) * (4 * nb * ld + 64);
   if (smem > 48 * 1024)
