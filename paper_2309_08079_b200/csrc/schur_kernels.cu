@@ -468,7 +468,7 @@ __global__ void k_block_cholesky(int K, int nb, const T* __restrict__ M, const T
 // order as the reference; within-block association differs (column sweeps),
 // so results agree to rounding (tests: 1e-10 of the oracle's cholesky_solve).
 template <class T, int NB>
-__global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* __restrict__ M,
+__global__ void __maxnreg__(144) k_block_thomas(int B, int K, const T* __restrict__ M,
                                                          const T* __restrict__ rhs, T* __restrict__ x,
                                                          T* __restrict__ factors, T* __restrict__ y,
                                                          int* __restrict__ status) {
@@ -476,9 +476,12 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
   constexpr int LD = NB + 1, NN = NB * NB, TS = NB * LD;
   __shared__ T sm[4][3 * TS + 2 * 16];
   const int hw = threadIdx.x >> 4, l = threadIdx.x & 15;
-  const unsigned mask = 0xffffu << (16 * ((threadIdx.x >> 4) & 1));
-  const int sys = blockIdx.x * 4 + hw;
-  if (sys >= B) return;  // whole half-warps
+  // full-warp shuffles / syncs (a constant mask: no divergence handling); a
+  // half-warp past the batch recomputes the last system and stores nothing
+  constexpr unsigned mask = 0xffffffffu;
+  const int sys_raw = blockIdx.x * 4 + hw;
+  bool live = sys_raw < B;  // false also once this system failed (keeps stepping, stores nothing)
+  const int sys = live ? sys_raw : B - 1;
   T* F = sm[hw];        // factor of Dhat_{i-1} (lower, row-major, ld LD)
   T* W = F + TS;        // Dhat_i, factorised in place (then swapped with F)
   T* X = W + TS;        // Dhat_{i-1}^-1 [L_i' | y_{i-1}]: column j = lane j
@@ -491,8 +494,8 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
   y += sys * D;
   factors += static_cast<size_t>(sys) * K * NN;
   status += sys;
-  const bool row = l < NB;
-  const int lr = row ? l : NB - 1;
+  const bool rowc = l < NB;  // rows that compute (stores: rowc && live)
+  const int lr = rowc ? l : NB - 1;
   auto blk = [&](int r, int s_) { return M + (static_cast<size_t>(r) * 3 + s_) * NN; };
   // In-place left-looking Cholesky of W (lane l: row l), Eigen's llt order;
   // returns the failing pivot (half-warp uniform) or -1.
@@ -508,30 +511,30 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
       const T sq = sqrt(piv <= T(0) ? T(1) : piv);
       const T rk = T(1) / sq;  // one division per pivot
       __syncwarp(mask);
-      if (row && l >= k) A[l * LD + k] = l == k ? sq : s * rk;
+      if (rowc && l >= k) A[l * LD + k] = l == k ? sq : s * rk;
       if (l == k) rd[k] = rk;
       __syncwarp(mask);
     }
     return fail;
   };
-  // F F' z = b for the calling lane's column b of X (in place, shared memory)
+  // F F' z = b for the calling lane's column b of X (in place, shared memory),
+  // in axpy form: each step finalises one entry and updates the rest, so the
+  // update chains are independent (no dot-product chains, few live loads)
   auto col_solve = [&](T* Z, const T* Fm, const T* rd) {
-    T z[NB];  // the column, kept in registers through both sweeps
+    T z[NB];
 #pragma unroll
     for (int r = 0; r < NB; ++r) z[r] = Z[r * LD];
 #pragma unroll
-    for (int r = 0; r < NB; ++r) {
-      T s = z[r];
+    for (int q = 0; q < NB; ++q) {
+      z[q] *= rd[q];
 #pragma unroll
-      for (int q = 0; q < r; ++q) s -= Fm[r * LD + q] * z[q];
-      z[r] = s * rd[r];
+      for (int r = q + 1; r < NB; ++r) z[r] -= Fm[r * LD + q] * z[q];
     }
 #pragma unroll
     for (int r = NB - 1; r >= 0; --r) {
-      T s = z[r];
+      z[r] *= rd[r];
 #pragma unroll
-      for (int q = r + 1; q < NB; ++q) s -= Fm[q * LD + r] * z[q];
-      z[r] = s * rd[r];
+      for (int q = 0; q < r; ++q) z[q] -= Fm[r * LD + q] * z[r];
     }
 #pragma unroll
     for (int r = 0; r < NB; ++r) Z[r * LD] = z[r];
@@ -542,7 +545,7 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
 #pragma unroll
     for (int r = 0; r < NB; ++r) {
       const T zr = __shfl_sync(mask, v, r, 16) * rd[r];
-      v = l == r ? zr : (l > r && row ? v - Fm[lr * LD + r] * zr : v);
+      v = l == r ? zr : (l > r && rowc ? v - Fm[lr * LD + r] * zr : v);
     }
 #pragma unroll
     for (int r = NB - 1; r >= 0; --r) {
@@ -556,19 +559,19 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + lr * NB + NB - 1));
   };
   // block 0
-  if (row)
+  if (rowc)
     for (int j = 0; j < NB; ++j) F[l * LD + j] = blk(0, 1)[l * NB + j];
-  T yv = row ? rhs[l] : T(0);
+  T yv = rowc ? rhs[l] : T(0);
   if (K > 1) {
     pf(blk(1, 0));
     pf(blk(1, 1));
   }
   __syncwarp(mask);
   if (chol(F, rdF) >= 0) {
-    if (l == 0) *status = 0;
-    return;
+    if (l == 0 && live) *status = 0;
+    live = false;
   }
-  if (row) {
+  if (rowc && live) {
     for (int j = 0; j < NB; ++j) factors[l * NB + j] = F[l * LD + j];
     y[l] = yv;
   }
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
       for (int q = 0; q < NB; ++q) {
         const T v = Li[q];
         const T yq = __shfl_sync(mask, yv, q, 16);
-        if (row) {
+        if (rowc) {
           X[q * LD + l] = v;
           W[l * LD + q] = v;
         }
@@ -594,13 +597,13 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
       pf(blk(i + 1, 0));
       pf(blk(i + 1, 1));
     }
-    if (row || l == NB) col_solve(X + l, F, rdF);
+    if (rowc || l == NB) col_solve(X + l, F, rdF);
     __syncwarp(mask);
     T Lrow[NB];  // row l of L_i
 #pragma unroll
-    for (int q = 0; q < NB; ++q) Lrow[q] = row ? W[l * LD + q] : T(0);
+    for (int q = 0; q < NB; ++q) Lrow[q] = rowc ? W[l * LD + q] : T(0);
     // y_i = rhs_i - L_i X[:, NB]; Dhat_i = D_i - L_i X[:, :NB] (into W)
-    T yi = row ? rhs[static_cast<size_t>(i) * NB + l] : T(0);
+    T yi = rowc ? rhs[static_cast<size_t>(i) * NB + l] : T(0);
     {
       T sy = T(0);
 #pragma unroll
@@ -613,15 +616,15 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
       T s = T(0);
 #pragma unroll
       for (int q = 0; q < NB; ++q) s += Lrow[q] * X[q * LD + j];
-      if (row) W[l * LD + j] = Dr[j] - s;
+      if (rowc) W[l * LD + j] = Dr[j] - s;
     }
     __syncwarp(mask);
     if (chol(W, rdW) >= 0) {
-      if (l == 0) *status = i;
-      return;
+      if (l == 0 && live) *status = i;
+      live = false;
     }
     yv = yi;
-    if (row) {
+    if (rowc && live) {
       T* Fo = factors + static_cast<size_t>(i) * NN;
       for (int j = 0; j < NB; ++j) Fo[l * NB + j] = W[l * LD + j];
       y[static_cast<size_t>(i) * NB + l] = yi;
@@ -640,14 +643,14 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
   T* xs = X;  // x_{i+1} for the R_i row products (shared by the half-warp)
   T xv = vec_solve(yv, F, rdF);  // lane l: element l of x_{K-1}
   for (int i = K - 2; i >= -1; --i) {
-    if (row) x[static_cast<size_t>(i + 1) * NB + l] = xv;
+    if (rowc && live) x[static_cast<size_t>(i + 1) * NB + l] = xv;
     if (i < 0) break;
     __syncwarp(mask);
     if (i > 0) {  // the next step's factor and R rows into L2
       pf(factors + static_cast<size_t>(i - 1) * NN);
       pf(blk(i - 1, 2));
     }
-    if (row) {
+    if (rowc && live) {
       xs[l] = xv;
       const T* Fi = factors + static_cast<size_t>(i) * NN;  // F <- factor i
       for (int j = 0; j < NB; ++j) F[l * LD + j] = Fi[l * NB + j];
@@ -655,7 +658,7 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
     }
     __syncwarp(mask);
     T v = T(0);
-    if (row) {
+    if (rowc && live) {
       const T* Rb = blk(i, 2) + l * NB;
       T s = T(0);
 #pragma unroll
@@ -665,7 +668,7 @@ __global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* _
     __syncwarp(mask);
     xv = vec_solve(v, F, rdF);
   }
-  if (l == 0) *status = -1;
+  if (l == 0 && live) *status = -1;
 }
 
 // ----------------------------------------------------------------- launchers
