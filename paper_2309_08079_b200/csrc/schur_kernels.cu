@@ -468,7 +468,7 @@ __global__ void k_block_cholesky(int K, int nb, const T* __restrict__ M, const T
 // order as the reference; within-block association differs (column sweeps),
 // so results agree to rounding (tests: 1e-10 of the oracle's cholesky_solve).
 template <class T, int NB>
-__global__ void __maxnreg__(144) k_block_thomas(int B, int K, const T* __restrict__ M,
+__global__ void __launch_bounds__(64, 7) k_block_thomas(int B, int K, const T* __restrict__ M,
                                                          const T* __restrict__ rhs, T* __restrict__ x,
                                                          T* __restrict__ factors, T* __restrict__ y,
                                                          int* __restrict__ status) {
