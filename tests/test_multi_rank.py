@@ -82,3 +82,45 @@ def test_two_rank_sharded_batch_equals_single_process(tmp_path, orc):
     want = np.stack([orc.solve(kb.system(i), PrecondKind.symmetric_stair, cfg=cfg).lambda_
                      for i in range(batch)])
     assert np.array_equal(lam, want)
+
+
+def _gpu_worker(rank, world, port, batch, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    import paper_2309_08079_b200.api as api
+    from paper_2309_08079_b200.types import PcgConfig, PrecondKind
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    first, last = shard_range(batch, world, rank)
+    # the bench's weak-scaling seeds: system i <- seed 2309 + i, on this rank's shard
+    kb = api.random_kkt_batch(2309 + first, last - first, 63, 14, 7)
+    lam, reps = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
+    t = max_over_ranks(float(rank + 1), dist)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (first, last, lam, list(reps.iterations)))
+    if rank == 0:
+        np.save(os.path.join(out_dir, "t.npy"), np.array([t]))
+        g = sorted(gathered, key=lambda g: g[0])
+        np.save(os.path.join(out_dir, "lam.npy"), np.concatenate([x[2] for x in g]))
+        np.save(os.path.join(out_dir, "it.npy"), np.concatenate([np.array(x[3]) for x in g]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_sharded_batch_on_the_device_path(tmp_path):
+    """World size 2 (gloo, both ranks on the test box's GPU) through libb2p's
+    solve_batched on contiguous shards: the gathered result equals the
+    single-process batch bitwise (the bench's N > 1 data path)."""
+    import paper_2309_08079_b200.api as api
+    from paper_2309_08079_b200.types import PcgConfig, PrecondKind
+    api.require_device()
+    batch, world = 300, 2
+    mp.spawn(_gpu_worker, args=(world, _free_port(), batch, str(tmp_path)), nprocs=world, join=True)
+    kb = api.random_kkt_batch(2309, batch, 63, 14, 7)
+    lam1, rep1 = api.solve_batched(kb, PrecondKind.symmetric_stair, 1, PcgConfig(epsilon=1e-8))
+    assert float(np.load(tmp_path / "t.npy")[0]) == 2.0
+    assert np.array_equal(np.load(tmp_path / "lam.npy"), lam1)
+    assert np.array_equal(np.load(tmp_path / "it.npy"), rep1.iterations)
