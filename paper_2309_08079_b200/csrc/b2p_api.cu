@@ -4,6 +4,7 @@
 // runs on the device or fails with B2P_CUDA_ERROR.
 #include <cuda_runtime.h>
 #include <immintrin.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -118,6 +119,13 @@ struct b2p_ctx {
 };
 
 namespace {
+
+// NVTX range per C-ABI call (header-only NVTX v3: a no-op unless a profiler
+// such as nsys / ncu --nvtx attaches), so timelines show the API boundary
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ errors
 struct Fail {
@@ -1558,6 +1566,7 @@ int b2p_blocktri_check(b2p_ctx* c, int dtype, int K, int nb, const void* M, doub
 // ---------------------------------------------------------------- schur
 int b2p_build_schur(b2p_ctx* c, int dtype, const b2p_kkt* k, void* S, void* gamma,
                     void* theta_inv, b2p_error* err) {
+  NvtxRange nvtx_("b2p_build_schur");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kkt(k);
@@ -1615,6 +1624,7 @@ int b2p_stair_matrix(b2p_ctx* c, int dtype, int K, int nb, const void* S, void* 
 int b2p_build_preconditioner(b2p_ctx* c, int dtype, int kind, int order, int K, int nb,
                              const void* S, const void* theta_inv, void* phi_inv,
                              b2p_error* err) {
+  NvtxRange nvtx_("b2p_build_preconditioner");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kind(kind, order);
@@ -1651,6 +1661,7 @@ int b2p_build_preconditioner(b2p_ctx* c, int dtype, int kind, int order, int K, 
 int b2p_apply_preconditioner(b2p_ctx* c, int dtype, int kind, int order, int K, int nb,
                              const void* S, const void* phi_inv, const void* r, int r_len,
                              void* out, b2p_error* err) {
+  NvtxRange nvtx_("b2p_apply_preconditioner");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kind(kind, order);
@@ -1706,6 +1717,7 @@ int b2p_pcg_solve(b2p_ctx* c, int dtype, int K, int nb, const void* S, int kind,
                   int phi_K, int phi_nb, const void* phi_inv, const void* gamma, int gamma_len,
                   const void* lambda0, int lambda0_len, const b2p_pcg_config* cfg,
                   void* lambda_out, b2p_solve_report* report, double* trace, b2p_error* err) {
+  NvtxRange nvtx_("b2p_pcg_solve");
   return guard(err, [&] {
     check_dtype(dtype);
     check_cfg(cfg);
@@ -1885,6 +1897,7 @@ extern "C" {
 int b2p_solve(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
               const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
               b2p_solve_report* report, double* trace, b2p_error* err) {
+  NvtxRange nvtx_("b2p_solve");
   return solve_one(c, dtype, k, kind, order, cfg, lambda0, lambda_out, nullptr, report, trace,
                    err);
 }
@@ -1893,6 +1906,7 @@ int b2p_sqp_step(b2p_ctx* c, int dtype, const b2p_kkt* k, int kind, int order,
                  const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out, void* dz_out,
                  b2p_solve_report* report, double* trace, b2p_error* err) {
   if (!dz_out) return guard(err, [] { throw invalid("sqp_step: null dz buffer"); });
+  NvtxRange nvtx_("b2p_sqp_step");
   return solve_one(c, dtype, k, kind, order, cfg, lambda0, lambda_out, dz_out, report, trace,
                    err);
 }
@@ -1924,6 +1938,7 @@ extern "C" {
 
 int b2p_reconstruct_primal(b2p_ctx* c, int dtype, const b2p_kkt* k, const void* lambda,
                            int lambda_len, void* dz_out, b2p_error* err) {
+  NvtxRange nvtx_("b2p_reconstruct_primal");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kkt(k);
@@ -1953,6 +1968,7 @@ int b2p_reconstruct_primal(b2p_ctx* c, int dtype, const b2p_kkt* k, const void* 
 
 int b2p_direct_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd,
                                     void* lambda_dev, int* status_dev, b2p_error* err) {
+  NvtxRange nvtx_("b2p_direct_solve_batched_device");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kkt(kd);
@@ -1984,6 +2000,7 @@ int b2p_direct_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_
 
 int b2p_reconstruct_primal_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd,
                                           const void* lambda_dev, void* dz_dev, b2p_error* err) {
+  NvtxRange nvtx_("b2p_reconstruct_primal_batched_device");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kkt(kd);
@@ -2002,6 +2019,7 @@ int b2p_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd
                              int order, const b2p_pcg_config* cfg, const void* lambda0_dev,
                              void* lambda_out_dev, b2p_solve_report* reports, int32_t* status_dev,
                              b2p_error* err) {
+  NvtxRange nvtx_("b2p_solve_batched_device");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kkt(kd);
@@ -2045,6 +2063,7 @@ int b2p_solve_batched_device(b2p_ctx* c, int dtype, int batch, const b2p_kkt* kd
 int b2p_solve_batched(b2p_ctx* c, int dtype, int batch, const b2p_kkt* k, int kind, int order,
                       const b2p_pcg_config* cfg, const void* lambda0, void* lambda_out,
                       b2p_solve_report* reports, b2p_error* err) {
+  NvtxRange nvtx_("b2p_solve_batched");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kkt(k);
@@ -2168,6 +2187,7 @@ int b2p_solve_batched_multi(const int* devices, int ndev, int dtype, int batch,
                             const b2p_kkt* k, int kind, int order, const b2p_pcg_config* cfg,
                             const void* lambda0, void* lambda_out, b2p_solve_report* reports,
                             b2p_error* err) {
+  NvtxRange nvtx_("b2p_solve_batched_multi");
   return guard(err, [&] {
     check_dtype(dtype);
     check_kkt(k);
