@@ -808,21 +808,26 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     const size_t eQ = size_t(K) * np * np, eq = size_t(K) * np, eR = size_t(N) * mp * mp,
                  er = size_t(N) * mp, eA = size_t(N) * np * np, eB = size_t(N) * np * mp,
                  ee = size_t(N) * np;
-    const size_t per = eQ + eq + eR + er + eA + eB + ee + 2 * np;
+    const bool padm = mp != m;  // (the control blocks travel as they are when m' = m)
+    const size_t per = eQ + eq + (padm ? eR + er : 0) + eA + eB + ee + 2 * np;
     T* w = static_cast<T*>(ws_get(c, tag + "xpad_kkt", sizeof(T) * per * B + 256));
-    T *Qp = w, *qp = Qp + eQ * B, *Rp = qp + eq * B, *rp_ = Rp + eR * B, *Ap = rp_ + er * B,
-      *Bp = Ap + eA * B, *ep = Bp + eB * B, *xsp = ep + ee * B, *x0p = xsp + size_t(np) * B;
+    T *Qp = w, *qp = Qp + eQ * B, *Rp = qp + eq * B, *rp_ = Rp + (padm ? eR * B : 0),
+      *Ap = rp_ + (padm ? er * B : 0), *Bp = Ap + eA * B, *ep = Bp + eB * B, *xsp = ep + ee * B,
+      *x0p = xsp + size_t(np) * B;
     reblock<T>(kv.Q, Qp, Bl * K, n, n, np, np, 1, st);
     reblock<T>(kv.q, qp, Bl * K, n, 1, np, 1, 0, st);
-    reblock<T>(kv.R, Rp, Bl * N, m, m, mp, mp, 1, st);
-    reblock<T>(kv.r, rp_, Bl * N, m, 1, mp, 1, 0, st);
+    if (padm) {
+      reblock<T>(kv.R, Rp, Bl * N, m, m, mp, mp, 1, st);
+      reblock<T>(kv.r, rp_, Bl * N, m, 1, mp, 1, 0, st);
+    }
     reblock<T>(kv.A, Ap, Bl * N, n, n, np, np, 0, st);
     reblock<T>(kv.B, Bp, Bl * N, n, m, np, mp, 0, st);
     reblock<T>(kv.e, ep, Bl * N, n, 1, np, 1, 0, st);
     reblock<T>(kv.x_s, xsp, Bl, n, 1, np, 1, 0, st);
     reblock<T>(kv.x0, x0p, Bl, n, 1, np, 1, 0, st);
-    f.Q = Qp, f.q = qp, f.R = Rp, f.r = rp_, f.A = Ap, f.Bm = Bp, f.e = ep, f.x_s = xsp,
-    f.x0 = x0p;
+    f.Q = Qp, f.q = qp, f.A = Ap, f.Bm = Bp, f.e = ep, f.x_s = xsp, f.x0 = x0p;
+    f.R = padm ? Rp : static_cast<const T*>(kv.R);
+    f.r = padm ? rp_ : static_cast<const T*>(kv.r);
     T* lam_pad = static_cast<T*>(ws_get(c, tag + "xpad_lam", sizeof(T) * B * K * np));
     if (lambda0) {
       T* l0p = static_cast<T*>(ws_get(c, tag + "xpad_l0", sizeof(T) * B * K * np));
@@ -830,7 +835,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
       f.lambda0 = l0p;
     }
     f.lambda_out = lam_pad;
-    c->launches += 9 + (lambda0 ? 1 : 0);
+    c->launches += (padm ? 9 : 7) + (lambda0 ? 1 : 0);
     return lam_pad;
   };
   if (use_fg) {
@@ -981,46 +986,17 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
   // real rows follow the unpadded recurrence (the dot products only gain
   // exact zero terms); lambda is cropped back.
   if (pad_ok) {
-    const int np = n + 1, m = k->m, N = K - 1;
+    const int np = n + 1, m = k->m;
     const long long Bl = B;
-    const size_t eQ = static_cast<size_t>(K) * np * np, eq = static_cast<size_t>(K) * np,
-                 eA = static_cast<size_t>(N) * np * np, eB = static_cast<size_t>(N) * np * m,
-                 ee = static_cast<size_t>(N) * np;
-    const size_t per = eQ + eq + eA + eB + ee + 2 * np;
-    T* w = static_cast<T*>(ws_get(c, tag + "pad_kkt", sizeof(T) * per * B + 256));
-    T *Qp = w, *qp = Qp + eQ * B, *Ap = qp + eq * B, *Bp = Ap + eA * B, *ep = Bp + eB * B,
-      *xsp = ep + ee * B, *x0p = xsp + static_cast<size_t>(np) * B;
-    reblock<T>(kv.Q, Qp, Bl * K, n, n, np, np, 1, st);
-    reblock<T>(kv.q, qp, Bl * K, n, 1, np, 1, 0, st);
-    reblock<T>(kv.A, Ap, Bl * N, n, n, np, np, 0, st);
-    reblock<T>(kv.B, Bp, Bl * N, n, m, np, m, 0, st);
-    reblock<T>(kv.e, ep, Bl * N, n, 1, np, 1, 0, st);
-    reblock<T>(kv.x_s, xsp, Bl, n, 1, np, 1, 0, st);
-    reblock<T>(kv.x0, x0p, Bl, n, 1, np, 1, 0, st);
-    T* lamp = static_cast<T*>(ws_get(c, tag + "pad_lam", sizeof(T) * B * K * np));
-    T* l0p = nullptr;
-    if (lambda0) {
-      l0p = static_cast<T*>(ws_get(c, tag + "pad_l0", sizeof(T) * B * K * np));
-      reblock<T>(lambda0, l0p, Bl * K, n, 1, np, 1, 0, st);
-    }
     const int grid = std::max(1, std::min(B, c->sm_count));
     FusedParams<T> f{};
     f.B = B;
     f.K = K;
     f.kind = kind;
-    f.Q = Qp;
-    f.q = qp;
-    f.R = static_cast<const T*>(kv.R);
-    f.r = static_cast<const T*>(kv.r);
-    f.A = Ap;
-    f.Bm = Bp;
-    f.e = ep;
-    f.x_s = xsp;
-    f.x0 = x0p;
+    f.lambda0 = static_cast<const T*>(lambda0);
+    T* lamp = pad_view(np, m, f);  // identity-padded state, control as it is
     f.slot = static_cast<T*>(
         ws_get(c, tag + "fused_slot", sizeof(T) * grid * fused_slot_elems<T>(K, np, m, false)));
-    f.lambda0 = l0p;
-    f.lambda_out = lamp;
     f.errkey = errkey;
     f.out = outs_dev;
     f.trace = trace_dev;
@@ -1045,7 +1021,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     }
     CK(launch_fused<T>(f, np, m, grid, st));
     reblock<T>(lamp, lambda_out, Bl * K, np, 1, n, 1, 0, st);
-    c->launches += 2 + (lambda0 ? 1 : 0) + 7;
+    c->launches += 2;
     c->last_path = 1;
     c->phases = time_it;
     if (time_it) CK(cudaEventRecord(c->ev1, st));
