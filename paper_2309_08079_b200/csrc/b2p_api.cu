@@ -788,6 +788,24 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
                                 : fg_pick_rp<T>(K, fnp, fmp, kind, c->sm_count,
                                                 env_int("B2P_FG_RP", 0));
   const bool fg_padded = fnp != n || fmp != k->m;
+  // fused kernels (one launch, no separate formation): a (start, formation end,
+  // end) event triple from the context's pool when the caller times phases
+  auto fused_timing_begin = [&]() {
+    if (!time_it) return;
+    if (!c->accounting) c->pool_used = 0;
+    if (c->pool_used + 3 > c->pool.size())
+      for (int q = 0; q < 3; ++q) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->pool.push_back(e);
+      }
+    c->ev0 = c->pool[c->pool_used];
+    c->ev2 = c->pool[c->pool_used + 1];
+    c->ev1 = c->pool[c->pool_used + 2];
+    c->pool_used += 3;
+    CK(cudaEventRecord(c->ev0, st));
+    CK(cudaEventRecord(c->ev2, st));
+  };
   // Single-solve policy (scripts/c1_policy_probe.py, profiles/r02_single_policy.json,
   // and the bench's c1 row): K <= 64 on one CTA (K 64: 87 us vs 93 on the grid
   // kernel; c1: 77 us in the bench vs 88 on the grid kernel there, although an
@@ -884,21 +902,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     sy.red = ll;
     sy.xt = ll + 2 * 16 * static_cast<size_t>(sy.gstride);
     sy.xr = sy.xt + 2 * static_cast<size_t>(sy.gstride) * 2 * 32;
-    if (time_it) {
-      if (!c->accounting) c->pool_used = 0;
-      if (c->pool_used + 3 > c->pool.size())
-        for (int q = 0; q < 3; ++q) {
-          cudaEvent_t e;
-          CK(cudaEventCreate(&e));
-          c->pool.push_back(e);
-        }
-      c->ev0 = c->pool[c->pool_used];
-      c->ev2 = c->pool[c->pool_used + 1];
-      c->ev1 = c->pool[c->pool_used + 2];
-      c->pool_used += 3;
-      CK(cudaEventRecord(c->ev0, st));
-      CK(cudaEventRecord(c->ev2, st));
-    }
+    fused_timing_begin();
     f.timing = env_int("B2P_PHASE_TIMING", 0)
                    ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 128ull * B))
                    : nullptr;
@@ -953,21 +957,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.epsilon = cfg ? cfg->epsilon : 1e-4;
     const int mi = cfg ? cfg->max_iter : 0;
     f.max_iter = mi > 0 ? mi : static_cast<int>(D);
-    if (time_it) {
-      if (!c->accounting) c->pool_used = 0;
-      if (c->pool_used + 3 > c->pool.size())
-        for (int q = 0; q < 3; ++q) {
-          cudaEvent_t e;
-          CK(cudaEventCreate(&e));
-          c->pool.push_back(e);
-        }
-      c->ev0 = c->pool[c->pool_used];
-      c->ev2 = c->pool[c->pool_used + 1];
-      c->ev1 = c->pool[c->pool_used + 2];
-      c->pool_used += 3;
-      CK(cudaEventRecord(c->ev0, st));
-      CK(cudaEventRecord(c->ev2, st));
-    }
+    fused_timing_begin();
     T* lam_pad = fc_padded ? pad_view(cnp, cmp, f) : nullptr;
     CK(launch_fc<T>(f, fcG, max_clusters, st, cnp));
     c->launches++;
@@ -1004,21 +994,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.epsilon = cfg ? cfg->epsilon : 1e-4;
     const int mi = cfg ? cfg->max_iter : 0;
     f.max_iter = mi > 0 ? mi : static_cast<int>(D);  // the unpadded dimension (resolve_max_iter)
-    if (time_it) {
-      if (!c->accounting) c->pool_used = 0;
-      if (c->pool_used + 3 > c->pool.size())
-        for (int q = 0; q < 3; ++q) {
-          cudaEvent_t e;
-          CK(cudaEventCreate(&e));
-          c->pool.push_back(e);
-        }
-      c->ev0 = c->pool[c->pool_used];
-      c->ev2 = c->pool[c->pool_used + 1];
-      c->ev1 = c->pool[c->pool_used + 2];
-      c->pool_used += 3;
-      CK(cudaEventRecord(c->ev0, st));
-      CK(cudaEventRecord(c->ev2, st));
-    }
+    fused_timing_begin();
     CK(launch_fused<T>(f, np, m, grid, st));
     reblock<T>(lamp, lambda_out, Bl * K, np, 1, n, 1, 0, st);
     c->launches += 2;
@@ -1060,21 +1036,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.epsilon = cfg ? cfg->epsilon : 1e-4;
     const int mi = cfg ? cfg->max_iter : 0;
     f.max_iter = mi > 0 ? mi : static_cast<int>(D);
-    if (time_it) {
-      if (!c->accounting) c->pool_used = 0;
-      if (c->pool_used + 3 > c->pool.size())
-        for (int q = 0; q < 3; ++q) {
-          cudaEvent_t e;
-          CK(cudaEventCreate(&e));
-          c->pool.push_back(e);
-        }
-      c->ev0 = c->pool[c->pool_used];
-      c->ev2 = c->pool[c->pool_used + 1];
-      c->ev1 = c->pool[c->pool_used + 2];
-      c->pool_used += 3;
-      CK(cudaEventRecord(c->ev0, st));
-      CK(cudaEventRecord(c->ev2, st));  // no separate formation launch
-    }
+    fused_timing_begin();
     CK(launch_fused<T>(f, n, k->m, grid, st));
     c->launches++;
     c->last_path = 1;
@@ -1111,21 +1073,7 @@ bool solve_device_impl(b2p_ctx* c, const b2p_kkt* k, const KktDev& kv, int B, in
     f.epsilon = cfg ? cfg->epsilon : 1e-4;
     const int mi = cfg ? cfg->max_iter : 0;
     f.max_iter = mi > 0 ? mi : static_cast<int>(D);
-    if (time_it) {
-      if (!c->accounting) c->pool_used = 0;
-      if (c->pool_used + 3 > c->pool.size())
-        for (int q = 0; q < 3; ++q) {
-          cudaEvent_t e;
-          CK(cudaEventCreate(&e));
-          c->pool.push_back(e);
-        }
-      c->ev0 = c->pool[c->pool_used];
-      c->ev2 = c->pool[c->pool_used + 1];
-      c->ev1 = c->pool[c->pool_used + 2];
-      c->pool_used += 3;
-      CK(cudaEventRecord(c->ev0, st));
-      CK(cudaEventRecord(c->ev2, st));
-    }
+    fused_timing_begin();
     f.timing = env_int("B2P_PHASE_TIMING", 0)
                    ? static_cast<unsigned long long*>(ws_get(c, "fused_timing", 128ull * B))
                    : nullptr;
