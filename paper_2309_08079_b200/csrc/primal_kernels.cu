@@ -415,9 +415,15 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (static_cast<int>(blockIdx.x) < nsc) {
+  // state and control CTAs interleaved (2c: state, 2c + 1: control while both
+  // remain), so every SM streams a mix of the heavy and the light tasks
+  const int ncc = (nu + kBulkTasks - 1) / kBulkTasks;
+  const int bx = static_cast<int>(blockIdx.x), mix = 2 * (nsc < ncc ? nsc : ncc);
+  const bool is_state = bx < mix ? (bx & 1) == 0 : nsc > ncc;
+  const int cta = bx < mix ? bx >> 1 : bx - mix / 2;  // index within its kind
+  if (is_state) {
     // ---- state solves: tasks t = t0 .. t0 + nt - 1, t = sys K + k
-    const int t0 = static_cast<int>(blockIdx.x) * kBulkTasks;
+    const int t0 = cta * kBulkTasks;
     const int nt = nx - t0 < kBulkTasks ? nx - t0 : kBulkTasks;
     // A blocks: a(t) = t - sys(t) for k < N; contiguous over the range
     const int sys0 = t0 / K;
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     }
   } else {
     // ---- control solves: tasks u = u0 .. u0 + nt - 1, u = sys N + k
-    const int u0 = (static_cast<int>(blockIdx.x) - nsc) * kBulkTasks;
+    const int u0 = cta * kBulkTasks;
     if (MB == 0 || u0 >= nu) return;
     const int nt = nu - u0 < kBulkTasks ? nu - u0 : kBulkTasks;
     // lambda_{k+1} blocks: index (u + sys + 1) over the range (contiguous)
