@@ -388,6 +388,10 @@ __device__ __forceinline__ void g8_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l) {
 // instead of per-lane row loads. The 8-lane groups then solve from shared
 // memory (Q_k's block doubles as its L tile).
 constexpr int kBulkTasks = 4;
+#ifndef B2P_PR_STAGE_A
+#define B2P_PR_STAGE_A 0
+#endif
+constexpr bool kPrStageA = B2P_PR_STAGE_A;
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned mbar) {
   asm volatile(
@@ -397,7 +401,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
-template <class T, int NB, int MB>
+template <class T, int NB, int MB, bool SA>
 __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(PrimalParams<T> p) {
   constexpr int H = NB / 2, NN = NB * NB;
   extern __shared__ __align__(16) unsigned char praw[];
@@ -433,15 +437,15 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     const int na = a_hi >= a_lo ? a_hi - a_lo + 1 : 0;
     const int nl = (nx - t0) < nt + 1 ? (nx - t0) : nt + 1;  // lambda blocks
     T* sQ = sm;                              // [16][NN] (then the L tiles)
-    T* sA = sQ + kBulkTasks * NN;            // [16][NN]
-    T* sq = sA + kBulkTasks * NN;            // [16][NB]
+    T* sA = sQ + kBulkTasks * NN;            // [16][NN] (SA: A_k staged; else read through L1)
+    T* sq = sA + (SA ? kBulkTasks * NN : 0);  // [16][NB]
     T* sl = sq + kBulkTasks * NB;            // [17][NB]
     if (threadIdx.x == 0) {
       const unsigned bq = static_cast<unsigned>(sizeof(T) * nt * NN), ba = static_cast<unsigned>(sizeof(T) * na * NN);
       const unsigned bv = static_cast<unsigned>(sizeof(T) * nt * NB), bl = static_cast<unsigned>(sizeof(T) * nl * NB);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bq + ba + bv + bl) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mb), "r"(bq + (SA ? ba : 0u) + bv + bl) : "memory");
       bulk_g2s(sQ, p.Q + static_cast<size_t>(t0) * NN, bq, mb);
-      if (na) bulk_g2s(sA, p.A + static_cast<size_t>(a_lo) * NN, ba, mb);
+      if (SA && na) bulk_g2s(sA, p.A + static_cast<size_t>(a_lo) * NN, ba, mb);
       bulk_g2s(sq, p.q + static_cast<size_t>(t0) * NB, bv, mb);
       bulk_g2s(sl, p.lambda + static_cast<size_t>(t0) * NB, bl, mb);
     }
@@ -466,15 +470,16 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     }
     T at0 = T(0), at1 = T(0);
     if (k < N) {  // (A_k' lambda_{k+1})_r = sum_c A_k(c, r) lambda_{k+1, c}
-      const T* Ab = sA + static_cast<size_t>(t - sys - a_lo) * NN;
+      auto ldA = [](const T* a) { return SA ? *a : __ldg(a); };
+      const T* Ab = SA ? sA + static_cast<size_t>(t - sys - a_lo) * NN : p.A + static_cast<size_t>(t - sys) * NN;
       const T* l1 = sl + static_cast<size_t>(j + 1) * NB;
 #pragma unroll
       for (int c = 0; c < NB; c += 2) {
         const double2 lv = *reinterpret_cast<const double2*>(l1 + c);
-        at0 += Ab[c * NB + lr] * lv.x;
-        at1 += Ab[c * NB + lr + H] * lv.x;
-        at0 += Ab[(c + 1) * NB + lr] * lv.y;
-        at1 += Ab[(c + 1) * NB + lr + H] * lv.y;
+        at0 += ldA(Ab + c * NB + lr) * lv.x;
+        at1 += ldA(Ab + c * NB + lr + H) * lv.x;
+        at0 += ldA(Ab + (c + 1) * NB + lr) * lv.y;
+        at1 += ldA(Ab + (c + 1) * NB + lr + H) * lv.y;
       }
     }
     const T* qk = sq + static_cast<size_t>(j) * NB;
@@ -483,7 +488,7 @@ __global__ void __launch_bounds__(8 * kBulkTasks) k_reconstruct_primal_bulk(Prim
     T r1 = -(qk[lr + H] + lk[lr + H] - at1);
     // duplicates work in place on their own copy? no: they share the last
     // task's block, so they factor in a scratch tile instead
-    T* Lt = tv ? Qb : sA + static_cast<size_t>(kBulkTasks - 1 - grp) * NN;
+    T* Lt = tv ? Qb : (SA ? sA + static_cast<size_t>(kBulkTasks - 1 - grp) * NN : sQ + static_cast<size_t>(grp) * NN);
     __syncthreads();  // every group has its rows; A blocks consumed (duplicates' scratch)
     g8x2_ldlt_solve<T, NB>(a0, a1, r0, r1, Lt, l);
     if (tv && l < H) {
@@ -573,7 +578,7 @@ cudaError_t launch_reconstruct_primal(const PrimalParams<T>& p, cudaStream_t st)
     const long long nx = static_cast<long long>(p.B) * (p.N + 1);
     const long long nu = static_cast<long long>(p.B) * p.N;
     const long long grid = (nx + kBulkTasks - 1) / kBulkTasks + (nu + kBulkTasks - 1) / kBulkTasks;
-    const size_t st_b = sizeof(T) * (2 * kBulkTasks * nb * nb + (2 * kBulkTasks + 1) * nb);
+    const size_t st_b = sizeof(T) * ((kPrStageA ? 2 : 1) * kBulkTasks * nb * nb + (2 * kBulkTasks + 1) * nb);
     const size_t ct_b = sizeof(T) * (kBulkTasks * nb * mbk + (kBulkTasks + 2 + kBulkTasks) * nb +
                                      2 * kBulkTasks * mbk * mbk + kBulkTasks * mbk) + 16;
     const size_t smem = st_b > ct_b ? st_b : ct_b;
@@ -586,7 +591,7 @@ cudaError_t launch_reconstruct_primal(const PrimalParams<T>& p, cudaStream_t st)
   if (tasks / kPrHw < 0x7fffffffLL) {
     if constexpr (sizeof(T) == 8) {
       if (p.n == 14 && p.m == 7 && tasks < 0x7fffffffLL && !std::getenv("B2P_PRIMAL_HW"))
-        return bulk_launch(k_reconstruct_primal_bulk<T, 14, 7>, 14, 7);  // 32-bit task indices
+        return bulk_launch(k_reconstruct_primal_bulk<T, 14, 7, kPrStageA>, 14, 7);  // 32-bit task indices
       if (p.n == 14 && p.m == 7) return hw_launch(k_reconstruct_primal_hw<T, 14, 7>);
     } else {
       if (p.n == 12 && p.m == 4) return hw_launch(k_reconstruct_primal_hw<T, 12, 4>);
