@@ -290,7 +290,7 @@ __device__ __forceinline__ void g8x2_ldlt_solve(T (&a0)[D], T (&a1)[D], T& r0, T
   constexpr int H = D / 2;
   const bool act = l < H;
   const int lr = act ? l : H - 1;
-  T d0 = T(1), d1 = T(1);
+  T rd0 = T(1), rd1 = T(1);  // 1 / d of this lane's rows
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     T s0 = T(0), s1 = a1[k];
@@ -304,50 +304,45 @@ __device__ __forceinline__ void g8x2_ldlt_solve(T (&a0)[D], T (&a1)[D], T& r0, T
     const T dk = __shfl_sync(0xffffffffu, k < H ? s0 : s1, k < H ? k : k - H, 8);
     const T rk = recip(dk);  // IEEE reciprocal: bitwise T(1) / dk
     if (k < H) {
-      if (lr == k) d0 = dk;
+      if (lr == k) rd0 = rk;
       if (act && lr > k) {
         Lt[lr * D + k] = s0;
         a0[k] = s0 * rk;
       }
     }
-    if (lr + H == k) d1 = dk;
+    if (lr + H == k) rd1 = rk;
     if (act && lr + H > k) {
       Lt[(lr + H) * D + k] = s1;
       a1[k] = s1 * rk;
     }
     __syncwarp();
   }
-  // L y = b (unit lower, column sweep), z = y / d
+  // L y = b (unit lower, column sweep)
 #pragma unroll
   for (int q = 0; q < D; ++q) {
     const T yq = __shfl_sync(0xffffffffu, q < H ? r0 : r1, q < H ? q : q - H, 8);
     if (lr > q) r0 -= a0[q] * yq;
     if (lr + H > q) r1 -= a1[q] * yq;
   }
-  r0 = r0 / d0;
-  r1 = r1 / d1;
-  if (act) {
-#pragma unroll
-    for (int q = 0; q < D; ++q) {
-      Lt[lr * D + q] = (q < lr) ? a0[q] : T(0);
-      Lt[(lr + H) * D + q] = (q < lr + H) ? a1[q] : T(0);
-    }
-  }
-  __syncwarp();
-  // L' x = z (transposed sweep through the unit-lower rows)
+  // L' x = y / d, transposed sweep on the factorisation's unscaled entries
+  // Lt(j, i) = L(j, i) d_i (i < j, stored above; no normalised copy of L is
+  // written back): x_i = (y_i - sum_{j > i} Lt(j, i) x_j) / d_i, and row j is
+  // final when the sweep reaches it
 #pragma unroll
   for (int j = D - 1; j >= 0; --j) {
-    const T xj = __shfl_sync(0xffffffffu, j < H ? r0 : r1, j < H ? j : j - H, 8);
+    const T xj = __shfl_sync(0xffffffffu, j < H ? r0 * rd0 : r1 * rd1, j < H ? j : j - H, 8);
     if (lr < j) r0 -= Lt[j * D + lr] * xj;
     if (lr + H < j) r1 -= Lt[j * D + lr + H] * xj;
   }
+  r0 *= rd0;
+  r1 *= rd1;
 }
 
 // the same on one row per lane (D <= 8; the control solve)
 template <class T, int D>
 __device__ __forceinline__ void g8_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l) {
   const int lr = l < D ? l : D - 1;
-  T dl = T(1);
+  T rdl = T(1);
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     T s = a[k];
@@ -355,7 +350,7 @@ __device__ __forceinline__ void g8_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l) {
     for (int q = 0; q < k; ++q) s -= a[q] * Lt[k * D + q];
     const T dk = __shfl_sync(0xffffffffu, s, k, 8);
     const T rk = recip(dk);  // IEEE reciprocal: bitwise T(1) / dk
-    if (lr == k) dl = dk;
+    if (lr == k) rdl = rk;
     if (l < D && lr > k) {
       Lt[lr * D + k] = s;
       a[k] = s * rk;
@@ -367,17 +362,13 @@ __device__ __forceinline__ void g8_ldlt_solve(T (&a)[D], T& rhs, T* Lt, int l) {
     const T yq = __shfl_sync(0xffffffffu, rhs, q, 8);
     if (lr > q) rhs -= a[q] * yq;
   }
-  rhs = rhs / dl;
-  if (l < D) {
-#pragma unroll
-    for (int q = 0; q < D; ++q) Lt[lr * D + q] = (q < lr) ? a[q] : T(0);
-  }
-  __syncwarp();
+  // L' x = y / d on the unscaled entries (as in g8x2_ldlt_solve)
 #pragma unroll
   for (int j = D - 1; j >= 0; --j) {
-    const T xj = __shfl_sync(0xffffffffu, rhs, j, 8);
+    const T xj = __shfl_sync(0xffffffffu, rhs * rdl, j, 8);
     if (lr < j) rhs -= Lt[j * D + lr] * xj;
   }
+  rhs *= rdl;
 }
 
 // ---------------------------------------------------------------------------
