@@ -293,14 +293,22 @@ __device__ __forceinline__ void g8x2_ldlt_solve(T (&a0)[D], T (&a1)[D], T& r0, T
   T rd0 = T(1), rd1 = T(1);  // 1 / d of this lane's rows
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    T s0 = T(0), s1 = a1[k];
+    T s0 = T(0), s1 = a1[k], u0 = T(0), u1 = T(0);
     if (k < H) s0 = a0[k];
+    // two partial sums per row (even / odd q): half the dependent FMA chain
 #pragma unroll
     for (int q = 0; q < k; ++q) {
       const T v = Lt[k * D + q];
-      if (k < H) s0 -= a0[q] * v;
-      s1 -= a1[q] * v;
+      if (q & 1) {
+        if (k < H) u0 -= a0[q] * v;
+        u1 -= a1[q] * v;
+      } else {
+        if (k < H) s0 -= a0[q] * v;
+        s1 -= a1[q] * v;
+      }
     }
+    s0 += u0;
+    s1 += u1;
     const T dk = __shfl_sync(0xffffffffu, k < H ? s0 : s1, k < H ? k : k - H, 8);
     const T rk = recip(dk);  // IEEE reciprocal: bitwise T(1) / dk
     if (k < H) {
